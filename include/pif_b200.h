@@ -1,0 +1,154 @@
+/*
+ * pif_b200.h — C ABI of the B200-native particle-decomposition PIF step.
+ *
+ * Plain C: device pointers, sizes and a cudaStream_t passed as void*.  No torch
+ * or C++ types cross this boundary.  Every entry point returns PIF_OK or an
+ * error code; pif_last_error() gives the message of the calling thread's last
+ * failure.  All launches are asynchronous on the given stream; nothing here
+ * synchronises the device except pif_plan_create/pif_plan_destroy.
+ *
+ * Each group cites the reference interface it replaces
+ * (/root/reference/pkg/src/pifsim/...; the "FFI" of the reference is its numba
+ * kernels in _kernels.py, called from nufft.py / pif.py / strategies.py).
+ *
+ * Layouts:
+ *   particles   structure of arrays (pif_soa_t), fp64, in HBM; id = int64
+ *   fine grid   n^3 fp64, flat index (ix*n + iy)*n + iz      (_kernels.py:48-54)
+ *   modes       (N,N,N) complex128 interleaved re/im, C order, m = index - N/2
+ *               (spectral.py:1-6)
+ *   field grid  n^3 x 4 fp64 interleaved (Ex, Ey, Ez, 0), plan-owned
+ */
+#ifndef PIF_B200_H
+#define PIF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PIF_OK 0
+#define PIF_ERR_VALUE 1       /* invalid argument: maps to ValueError          */
+#define PIF_ERR_CUDA 2        /* CUDA / cuFFT / allocation failure: RuntimeError */
+#define PIF_ERR_STATE 3       /* call out of order (e.g. no field solved yet)  */
+
+#define PIF_SHAPE_DELTA 0     /* pif.py:77-78 */
+#define PIF_SHAPE_CIC 1       /* pif.py:79-85 */
+#define PIF_EXT_NONE 0        /* pif.py:50-51 */
+#define PIF_EXT_QUADRUPOLE 1  /* pif.py:52-57 */
+
+typedef struct pif_plan_s *pif_plan_t;
+
+/* Particle view (structure of arrays, device memory, `count` particles). */
+typedef struct {
+    double *x, *y, *z;
+    double *vx, *vy, *vz;
+    int64_t *id;
+    int64_t count;
+} pif_soa_t;
+
+const char *pif_last_error(void);
+int pif_abi_version(void);
+
+/* ---- plan: replaces nufft.make_plan / NufftPlan (nufft.py:43-84) ----------
+ * All scalars and (N,) tables are computed on the host by the caller exactly
+ * as the reference computes them (numpy), so the device sees identical
+ * constants; the plan owns the cuFFT plans, the fine
+ * grid, spectra, the interleaved field grid and the cell tables on `device`. */
+typedef struct {
+    int N;                   /* modes per dimension (even, >= 4)               */
+    double L;                /* periodic box length                            */
+    double eps;              /* NUFFT tolerance                                */
+    int w;                   /* window width  ceil(|log10 eps|) + 1 (nufft.py:79) */
+    double beta;             /* 2.30 w (nufft.py:81)                           */
+    int n_up;                /* fine grid per dimension (nufft.py:82-83)        */
+    const double *deconv;    /* host (N,) 1/psi_hat (nufft.py:57, 87-102)      */
+    const double *kvec;      /* host (N,) 2 pi/L * m (spectral.py:57-60)       */
+    const double *shape_cic; /* host (N,) cloud-in-cell S_k (pif.py:79-85)     */
+    double inv_L3;           /* 1.0 / L**3 (pif.py:101)                        */
+    double half_L3;          /* 0.5 * L**3 (spectral.py:91)                    */
+} pif_plan_desc_t;
+
+int pif_plan_create(const pif_plan_desc_t *desc, int device, pif_plan_t *out);
+int pif_plan_destroy(pif_plan_t plan);
+/* Bytes of device memory owned by the plan. */
+int64_t pif_plan_device_bytes(pif_plan_t plan);
+
+/* ---- binning (new; the reference spreads in particle order, _kernels.py:73) -
+ * pif_bin_keys: per-particle ES-stencil cell key ((i0x*n + i0y)*n + i0z, each
+ * i0 = ceil(x/h - w/2) mod n as in _kernels.py:19) plus its rank inside the
+ * cell; counts accumulate in the plan's cell table.  Positions must already
+ * lie in [0, L) (pif_wrap_points does that, nufft.py:105-113).
+ * pif_bin_scatter: exclusive scan of the counts, then scatter src -> dst in
+ * cell order; dst is what the *_sorted kernels read.  Resets the counts. */
+int pif_wrap_points(pif_plan_t plan, double *x, double *y, double *z, int64_t M, void *stream);
+int pif_bin_keys(pif_plan_t plan, const pif_soa_t *src, int32_t *key, int32_t *rank,
+                 void *stream);
+int pif_bin_scatter(pif_plan_t plan, const pif_soa_t *src, pif_soa_t *dst, const int32_t *key,
+                    const int32_t *rank, int with_velocity, void *stream);
+
+/* ---- type-1 spreading: replaces _kernels.spread_r (_kernels.py:57-96) ------
+ * Reads cell-sorted particles (dst of pif_bin_scatter).  strengths == NULL
+ * means the uniform charge q (strategies.py:160-161); otherwise strengths is
+ * indexed by particle id.  Overwrites the plan's fine grid. */
+int pif_spread_sorted(pif_plan_t plan, const pif_soa_t *sorted, const double *strengths,
+                      double q, void *stream);
+
+/* ---- uniform FFT + truncate/deconvolve: replaces nufft.py:140-145 ----------
+ * D2Z of the plan's fine grid (cuFFT), then modes = F[m mod n] * d(mx)d(my)d(mz) / n^3
+ * into `modes` (complex N^3, caller-owned, e.g. the allreduce buffer). */
+int pif_grid_to_modes(pif_plan_t plan, double *modes, void *stream);
+
+/* ---- field solve: replaces pif.finish_deposit (pif.py:95-105),
+ * spectral.poisson_efield (spectral.py:63-82), field_energy (spectral.py:85-91),
+ * the Hermitian guard (pif.py:128-133, spectral.py:94-101) and
+ * nufft._padded_spectrum + 3x ifftn (nufft.py:148-156, 182-185).
+ * Input: the allreduced raw type-1 modes.  Output: rho (optional, complex N^3),
+ * the plan's interleaved field grid, and scalars[0..2] (device) =
+ * {field energy W, max Hermitian mismatch over Ex,Ey,Ez relative to each scale,
+ *  unused}.  shape is PIF_SHAPE_*. */
+int pif_solve_fields(pif_plan_t plan, const double *raw_modes, int shape, double *rho_out,
+                     double *scalars, void *stream);
+/* Same, from caller-supplied E modes (gather_efield API, pif.py:115-137):
+ * guard value into scalars[1], no energy. */
+int pif_fields_from_modes(pif_plan_t plan, const double *ex, const double *ey, const double *ez,
+                          int shape, double *scalars, void *stream);
+/* Field energy only (spectral.field_energy of poisson_efield(rho)) for a
+ * finished rho: scalars[0] = W. */
+int pif_field_energy(pif_plan_t plan, const double *rho, double *scalars, void *stream);
+/* Poisson solve only (spectral.poisson_efield): rho -> Ex, Ey, Ez (complex N^3). */
+int pif_poisson(pif_plan_t plan, const double *rho, double *ex, double *ey, double *ez,
+                void *stream);
+
+/* ---- type-2 gather fused with the Boris push: replaces _kernels.interp_r3
+ * (_kernels.py:125-183) + pif.boris_push (pif.py:140-158) +
+ * pif.external_field_eval (pif.py:43-57) + particles.wrap_positions.
+ * Updates the sorted particles in place, emits the next cell key and rank
+ * (pif_bin_keys semantics) and writes diag[0..5] = {sum v.v, sum vx, sum vy,
+ * sum vz, sum phi_ext(x), 0} over the updated particles (device, overwritten;
+ * the caller scales by m/2, m, q as pif.py:60-68, 240-245 do).
+ * half = 0.5*dt*qm and the Boris constants (tq = half*B, sq = 2 tq/(1+tq.tq))
+ * are computed by the caller exactly as pif.py:146-153 does; has_b == 0 skips
+ * the rotation. */
+int pif_interp_push(pif_plan_t plan, pif_soa_t *sorted, double half, double dt,
+                    const double tq[3], const double sq[3], int has_b, int e_kind,
+                    int32_t *key, int32_t *rank, double *diag, void *stream);
+/* Gather only (gather_efield): E at the sorted particles written to
+ * E_out[3*id + d] (AoS, particle id order). */
+int pif_interp_sorted(pif_plan_t plan, const pif_soa_t *sorted, double *E_out, void *stream);
+/* Diagnostic sums of a particle set (Recorder.record, strategies.py:96-106). */
+int pif_particle_diag(pif_plan_t plan, const pif_soa_t *p, int e_kind, double *diag,
+                      void *stream);
+
+/* ---- complex variants for the type1/type2 API (_kernels.py:31-54, 99-122) --
+ * pts are AoS (M,3) device doubles already wrapped into [0,L). */
+int pif_type1_complex(pif_plan_t plan, const double *pts, const double *vals, int64_t M,
+                      double *modes, void *stream);
+int pif_type2_complex(pif_plan_t plan, const double *modes, const double *pts, int64_t M,
+                      double *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIF_B200_H */

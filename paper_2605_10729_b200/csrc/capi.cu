@@ -1,0 +1,343 @@
+// C ABI of libpifb200 (include/pif_b200.h): plan lifetime, argument checks,
+// device selection and dispatch to the kernel launchers.
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "pif_internal.cuh"
+
+namespace pif {
+
+static thread_local std::string g_error;
+
+void set_error(const std::string &msg) { g_error = msg; }
+
+int fail_cuda(cudaError_t e, const char *where) {
+    if (e == cudaSuccess) return PIF_OK;
+    set_error(std::string(where) + ": " + cudaGetErrorString(e));
+    return PIF_ERR_CUDA;
+}
+
+int fail_cufft(cufftResult r, const char *where) {
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), "%s: cufft error %d", where, (int)r);
+    set_error(buf);
+    return PIF_ERR_CUDA;
+}
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+template <typename T>
+int dalloc(Plan &p, T **ptr, size_t count) {
+    cudaError_t e = cudaMalloc(reinterpret_cast<void **>(ptr), sizeof(T) * count);
+    if (e != cudaSuccess) return fail_cuda(e, "cudaMalloc");
+    p.bytes += (int64_t)(sizeof(T) * count);
+    return PIF_OK;
+}
+
+void release(Plan &p) {
+    void *ptrs[] = {p.deconv, p.kvec, p.grid, p.spec, p.field, p.field3, p.emodes, p.cgrid,
+                    p.cell_count, p.cell_start, p.scan_tmp, p.work, p.partials, p.maxbits,
+                    p.shape_tab};
+    for (void *q : ptrs)
+        if (q) cudaFree(q);
+    if (p.d2z) cufftDestroy(p.d2z);
+    if (p.z2d3) cufftDestroy(p.z2d3);
+    if (p.z2z) cufftDestroy(p.z2z);
+}
+
+bool soa_ok(const pif_soa_t *s, bool vel) {
+    if (!s || s->count < 0) return false;
+    if (s->count == 0) return true;
+    if (!s->x || !s->y || !s->z || !s->id) return false;
+    if (vel && (!s->vx || !s->vy || !s->vz)) return false;
+    return s->count < (int64_t)INT32_MAX;
+}
+
+int bad(const char *msg) {
+    set_error(msg);
+    return PIF_ERR_VALUE;
+}
+
+}  // namespace
+
+int ensure_complex(Plan &p) {
+    if (p.cgrid) return PIF_OK;
+    DeviceGuard g(p.device);
+    int rc = dalloc(p, &p.cgrid, p.n3);
+    if (rc != PIF_OK) return rc;
+    cufftResult r = cufftPlan3d(&p.z2z, p.n, p.n, p.n, CUFFT_Z2Z);
+    if (r != CUFFT_SUCCESS) return fail_cufft(r, "cufftPlan3d(Z2Z)");
+    return PIF_OK;
+}
+
+}  // namespace pif
+
+using pif::Plan;
+
+struct pif_plan_s {
+    Plan p;
+};
+
+extern "C" {
+
+const char *pif_last_error(void) { return pif::g_error.c_str(); }
+
+int pif_abi_version(void) { return 1; }
+
+int pif_plan_create(const pif_plan_desc_t *d, int device, pif_plan_t *out) {
+    if (!d || !out) return pif::bad("null plan descriptor");
+    *out = nullptr;
+    if (d->N < 4 || d->N % 2) return pif::bad("N must be even and >= 4");
+    if (!(d->L > 0) || !std::isfinite(d->L)) return pif::bad("invalid L");
+    if (d->w < 2 || d->w > pif::kMaxW) return pif::bad("window width out of range");
+    if (d->n_up < d->N || d->n_up % 2 || d->n_up < d->w) return pif::bad("invalid n_up");
+    if ((int64_t)d->n_up * d->n_up * d->n_up >= (int64_t)INT32_MAX)
+        return pif::bad("fine grid too large for 32-bit cell keys");
+    if (!d->deconv || !d->kvec || !d->shape_cic) return pif::bad("missing host tables");
+    pif::DeviceGuard guard(device);
+    if (!guard.ok) return pif::fail_cuda(cudaErrorInvalidDevice, "cudaSetDevice");
+    pif_plan_s *h = new (std::nothrow) pif_plan_s;
+    if (!h) return pif::bad("out of host memory");
+    Plan &p = h->p;
+    p.N = d->N;
+    p.n = d->n_up;
+    p.w = d->w;
+    p.device = device;
+    p.L = d->L;
+    p.eps = d->eps;
+    p.beta = d->beta;
+    p.h = d->L / d->n_up;  // NufftPlan.h (nufft.py:60-63)
+    p.inv_L3 = d->inv_L3;
+    p.half_L3 = d->half_L3;
+    p.n3 = (int64_t)p.n * p.n * p.n;
+    p.nhalf = (int64_t)p.n * p.n * (p.n / 2 + 1);
+    const int64_t N3 = (int64_t)p.N * p.N * p.N;
+    cudaDeviceGetAttribute(&p.sm_count, cudaDevAttrMultiProcessorCount, device);
+    p.partial_blocks = p.sm_count * 32;
+    int rc = PIF_OK;
+#define TRY(x)                    \
+    do {                          \
+        rc = (x);                 \
+        if (rc != PIF_OK) goto fail; \
+    } while (0)
+    TRY(pif::dalloc(p, &p.deconv, p.N));
+    TRY(pif::dalloc(p, &p.kvec, p.N));
+    TRY(pif::dalloc(p, &p.shape_tab, 2 * p.N));
+    TRY(pif::dalloc(p, &p.grid, p.n3));
+    TRY(pif::dalloc(p, &p.spec, 3 * p.nhalf));
+    TRY(pif::dalloc(p, &p.field, 4 * p.n3));
+    TRY(pif::dalloc(p, &p.emodes, 3 * N3));
+    TRY(pif::dalloc(p, &p.cell_count, p.n3 + 1));
+    TRY(pif::dalloc(p, &p.cell_start, p.n3 + 1));
+    TRY(pif::dalloc(p, &p.work, 4));
+    TRY(pif::dalloc(p, &p.partials, (size_t)p.partial_blocks * pif::kDiagSlots));
+    TRY(pif::dalloc(p, &p.maxbits, 8));
+    {
+        cudaError_t e = cudaMemcpy(p.deconv, d->deconv, sizeof(double) * p.N, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess)
+            e = cudaMemcpy(p.kvec, d->kvec, sizeof(double) * p.N, cudaMemcpyHostToDevice);
+        double *ones = new double[p.N];
+        for (int i = 0; i < p.N; ++i) ones[i] = 1.0;
+        if (e == cudaSuccess)
+            e = cudaMemcpy(p.shape_tab, ones, sizeof(double) * p.N, cudaMemcpyHostToDevice);
+        delete[] ones;
+        if (e == cudaSuccess)
+            e = cudaMemcpy(p.shape_tab + p.N, d->shape_cic, sizeof(double) * p.N,
+                           cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemset(p.cell_count, 0, sizeof(int32_t) * (p.n3 + 1));
+        if (e == cudaSuccess) e = cudaMemset(p.field, 0, sizeof(double) * 4 * p.n3);
+        if (e != cudaSuccess) {
+            rc = pif::fail_cuda(e, "plan tables");
+            goto fail;
+        }
+        size_t tmp = 0;
+        e = cub::DeviceScan::ExclusiveSum(nullptr, tmp, p.cell_count, p.cell_start,
+                                          (int)(p.n3 + 1));
+        if (e != cudaSuccess) {
+            rc = pif::fail_cuda(e, "scan sizing");
+            goto fail;
+        }
+        p.scan_tmp_bytes = tmp;
+        TRY(pif::dalloc(p, reinterpret_cast<char **>(&p.scan_tmp), tmp));
+    }
+    {
+        cufftResult r = cufftPlan3d(&p.d2z, p.n, p.n, p.n, CUFFT_D2Z);
+        if (r != CUFFT_SUCCESS) {
+            rc = pif::fail_cufft(r, "cufftPlan3d(D2Z)");
+            goto fail;
+        }
+        int dims[3] = {p.n, p.n, p.n};
+        int inembed[3] = {p.n, p.n, p.n / 2 + 1};
+        int onembed[3] = {p.n, p.n, p.n};
+        // Z2D straight into the interleaved (Ex,Ey,Ez,0) grid: ostride 4, odist 1
+        r = cufftPlanMany(&p.z2d3, 3, dims, inembed, 1, (int)p.nhalf, onembed, 4, 1, CUFFT_Z2D, 3);
+        if (r == CUFFT_SUCCESS) {
+            p.z2d_strided = true;
+        } else {
+            p.z2d3 = 0;
+            r = cufftPlanMany(&p.z2d3, 3, dims, inembed, 1, (int)p.nhalf, onembed, 1, (int)p.n3,
+                              CUFFT_Z2D, 3);
+            if (r != CUFFT_SUCCESS) {
+                rc = pif::fail_cufft(r, "cufftPlanMany(Z2D)");
+                goto fail;
+            }
+            TRY(pif::dalloc(p, &p.field3, 3 * p.n3));
+        }
+    }
+#undef TRY
+    *out = h;
+    return PIF_OK;
+fail:
+    pif::release(p);
+    delete h;
+    return rc;
+}
+
+int pif_plan_destroy(pif_plan_t plan) {
+    if (!plan) return PIF_OK;
+    {
+        pif::DeviceGuard g(plan->p.device);
+        cudaDeviceSynchronize();
+        pif::release(plan->p);
+    }
+    delete plan;
+    return PIF_OK;
+}
+
+int64_t pif_plan_device_bytes(pif_plan_t plan) { return plan ? plan->p.bytes : 0; }
+
+#define PLAN_CHECK()                                          \
+    if (!plan) return pif::bad("null plan");                  \
+    Plan &p = plan->p;                                        \
+    pif::DeviceGuard guard_(p.device);                        \
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+
+int pif_wrap_points(pif_plan_t plan, double *x, double *y, double *z, int64_t M, void *stream) {
+    PLAN_CHECK();
+    if (M < 0 || (M > 0 && (!x || !y || !z))) return pif::bad("invalid points");
+    return pif::launch_wrap(p, x, y, z, M, s);
+}
+
+int pif_bin_keys(pif_plan_t plan, const pif_soa_t *src, int32_t *key, int32_t *rank,
+                 void *stream) {
+    PLAN_CHECK();
+    if (!pif::soa_ok(src, false)) return pif::bad("invalid particle view");
+    if (src->count > 0 && (!key || !rank)) return pif::bad("missing key/rank buffers");
+    return pif::launch_bin_keys(p, *src, key, rank, s);
+}
+
+int pif_bin_scatter(pif_plan_t plan, const pif_soa_t *src, pif_soa_t *dst, const int32_t *key,
+                    const int32_t *rank, int with_velocity, void *stream) {
+    PLAN_CHECK();
+    if (!pif::soa_ok(src, with_velocity) || !dst) return pif::bad("invalid particle view");
+    pif_soa_t d = *dst;
+    d.count = src->count;
+    if (!pif::soa_ok(&d, with_velocity)) return pif::bad("invalid destination view");
+    int rc = pif::launch_bin_scatter(p, *src, d, key, rank, with_velocity != 0, s);
+    dst->count = d.count;
+    return rc;
+}
+
+int pif_spread_sorted(pif_plan_t plan, const pif_soa_t *sorted, const double *strengths,
+                      double q, void *stream) {
+    PLAN_CHECK();
+    if (!pif::soa_ok(sorted, false)) return pif::bad("invalid particle view");
+    return pif::launch_spread(p, *sorted, strengths, q, s);
+}
+
+int pif_grid_to_modes(pif_plan_t plan, double *modes, void *stream) {
+    PLAN_CHECK();
+    if (!modes) return pif::bad("null modes");
+    return pif::launch_modes_from_spec(p, modes, s);
+}
+
+int pif_solve_fields(pif_plan_t plan, const double *raw_modes, int shape, double *rho_out,
+                     double *scalars, void *stream) {
+    PLAN_CHECK();
+    if (!raw_modes || !scalars) return pif::bad("null modes/scalars");
+    if (shape != PIF_SHAPE_DELTA && shape != PIF_SHAPE_CIC) return pif::bad("unknown shape");
+    return pif::launch_solve_fields(p, raw_modes, shape, rho_out, scalars, true, nullptr, nullptr,
+                                    nullptr, s);
+}
+
+int pif_fields_from_modes(pif_plan_t plan, const double *ex, const double *ey, const double *ez,
+                          int shape, double *scalars, void *stream) {
+    PLAN_CHECK();
+    if (!ex || !ey || !ez || !scalars) return pif::bad("null E modes/scalars");
+    if (shape != PIF_SHAPE_DELTA && shape != PIF_SHAPE_CIC) return pif::bad("unknown shape");
+    return pif::launch_solve_fields(p, nullptr, shape, nullptr, scalars, false, ex, ey, ez, s);
+}
+
+int pif_field_energy(pif_plan_t plan, const double *rho, double *scalars, void *stream) {
+    PLAN_CHECK();
+    if (!rho || !scalars) return pif::bad("null rho/scalars");
+    return pif::launch_field_energy(p, rho, scalars, s);
+}
+
+int pif_poisson(pif_plan_t plan, const double *rho, double *ex, double *ey, double *ez,
+                void *stream) {
+    PLAN_CHECK();
+    if (!rho || !ex || !ey || !ez) return pif::bad("null rho/E");
+    return pif::launch_poisson(p, rho, ex, ey, ez, s);
+}
+
+int pif_interp_push(pif_plan_t plan, pif_soa_t *sorted, double half, double dt,
+                    const double tq[3], const double sq[3], int has_b, int e_kind,
+                    int32_t *key, int32_t *rank, double *diag, void *stream) {
+    PLAN_CHECK();
+    if (!pif::soa_ok(sorted, true)) return pif::bad("invalid particle view");
+    if (sorted->count > 0 && (!key || !rank)) return pif::bad("missing key/rank buffers");
+    if (!diag) return pif::bad("null diag");
+    if (e_kind != PIF_EXT_NONE && e_kind != PIF_EXT_QUADRUPOLE) return pif::bad("unknown e_kind");
+    if (!(dt > 0)) return pif::bad("dt must be positive");
+    return pif::launch_interp(p, *sorted, true, half, dt, tq, sq, has_b, e_kind, key, rank, diag,
+                              nullptr, s);
+}
+
+int pif_interp_sorted(pif_plan_t plan, const pif_soa_t *sorted, double *E_out, void *stream) {
+    PLAN_CHECK();
+    if (!pif::soa_ok(sorted, false)) return pif::bad("invalid particle view");
+    if (sorted->count > 0 && !E_out) return pif::bad("null E_out");
+    pif_soa_t v = *sorted;
+    return pif::launch_interp(p, v, false, 0.0, 1.0, nullptr, nullptr, 0, PIF_EXT_NONE, nullptr,
+                              nullptr, nullptr, E_out, s);
+}
+
+int pif_particle_diag(pif_plan_t plan, const pif_soa_t *ps, int e_kind, double *diag,
+                      void *stream) {
+    PLAN_CHECK();
+    if (!pif::soa_ok(ps, true) || !diag) return pif::bad("invalid particle view");
+    return pif::launch_particle_diag(p, *ps, e_kind, diag, s);
+}
+
+int pif_type1_complex(pif_plan_t plan, const double *pts, const double *vals, int64_t M,
+                      double *modes, void *stream) {
+    PLAN_CHECK();
+    if (M < 0 || (M > 0 && (!pts || !vals)) || !modes) return pif::bad("invalid type1 arguments");
+    return pif::launch_type1_complex(p, pts, vals, M, modes, s);
+}
+
+int pif_type2_complex(pif_plan_t plan, const double *modes, const double *pts, int64_t M,
+                      double *out, void *stream) {
+    PLAN_CHECK();
+    if (M < 0 || (M > 0 && (!pts || !out)) || !modes) return pif::bad("invalid type2 arguments");
+    return pif::launch_type2_complex(p, modes, pts, M, out, s);
+}
+
+}  // extern "C"

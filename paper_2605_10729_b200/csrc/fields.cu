@@ -1,0 +1,385 @@
+// Mode-space kernels of the PD-PIF step: truncate + deconvolve after the D2Z
+// (nufft.py:140-145), finish_deposit (pif.py:95-105), Poisson E_k = -i k rho/|k|^2
+// (spectral.py:63-82), Parseval field energy (spectral.py:85-91), the Hermitian
+// guard (spectral.py:94-101, pif.py:128-133), and the padded spectra of the three
+// field components (nufft.py:148-156) written as Hermitian-symmetrised half
+// spectra so one batched Z2D reproduces Re(ifftn(pad)) (nufft.py:184-185).
+// All of this is O(N^3) or O(n^3) per step; the particle kernels dominate.
+#include "pif_internal.cuh"
+
+namespace pif {
+
+namespace {
+
+__device__ __forceinline__ double2 cscale(double2 a, double s) {
+    return make_double2(__dmul_rn(a.x, s), __dmul_rn(a.y, s));
+}
+
+__device__ __forceinline__ double block_sum(double v, double *scratch) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum(v);
+    if (lane == 0) scratch[wid] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < nw; ++i) s += scratch[i];
+    __syncthreads();
+    return s;
+}
+
+// m mod n -> mode index (m + N/2) of a fine-grid frequency, or -1 outside the band
+__device__ __forceinline__ int band_index(int f, int N, int n) {
+    if (f < N / 2) return f + N / 2;
+    if (f >= n - N / 2) return f - n + N / 2;
+    return -1;
+}
+
+// (1) truncate the D2Z half spectrum to the (N,N,N) mode block and deconvolve
+__global__ void modes_from_spec_kernel(const double2 *__restrict__ spec,
+                                       const double *__restrict__ deconv, double2 *__restrict__ out,
+                                       int N, int n, double inv_n3) {
+    const int64_t N3 = (int64_t)N * N * N;
+    const int nh1 = n / 2 + 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N3;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int iz = (int)(i % N), iy = (int)((i / N) % N), ix = (int)(i / ((int64_t)N * N));
+        const int fx = pmod(ix - N / 2, n), fy = pmod(iy - N / 2, n), fz = pmod(iz - N / 2, n);
+        double2 v;
+        if (fz <= n / 2) {
+            v = spec[((int64_t)fx * n + fy) * nh1 + fz];
+        } else {  // F(f) = conj F(-f) for a real grid
+            const double2 c = spec[((int64_t)((n - fx) % n) * n + (n - fy) % n) * nh1 + (n - fz)];
+            v = make_double2(c.x, -c.y);
+        }
+        // block *= d[:,None,None]; *= d[None,:,None]; *= d[None,None,:]; *= 1/n^3
+        v = cscale(v, deconv[ix]);
+        v = cscale(v, deconv[iy]);
+        v = cscale(v, deconv[iz]);
+        v = cscale(v, inv_n3);
+        out[i] = v;
+    }
+}
+
+// (2) finish_deposit + Poisson + energy partials.  mode 0: raw -> rho (shape,
+// 1/L^3, k=0 zeroed); mode 1: input is already rho.  E written unshaped.
+__global__ void poisson_kernel(const double2 *__restrict__ in, int from_raw,
+                               const double *__restrict__ shape, double inv_L3,
+                               const double *__restrict__ kvec, double2 *__restrict__ rho_out,
+                               double2 *__restrict__ ex, double2 *__restrict__ ey,
+                               double2 *__restrict__ ez, double *__restrict__ partials, int N) {
+    __shared__ double scratch[32];
+    const int64_t N3 = (int64_t)N * N * N;
+    const int64_t mid = ((int64_t)(N / 2) * N + N / 2) * N + N / 2;
+    double en = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N3;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int iz = (int)(i % N), iy = (int)((i / N) % N), ix = (int)(i / ((int64_t)N * N));
+        double2 r = in[i];
+        if (from_raw) {
+            r = cscale(r, shape[ix]);
+            r = cscale(r, shape[iy]);
+            r = cscale(r, shape[iz]);
+            r = cscale(r, inv_L3);
+            if (i == mid) r = make_double2(0.0, 0.0);
+            if (rho_out) rho_out[i] = r;
+        }
+        const double kx = kvec[ix], ky = kvec[iy], kz = kvec[iz];
+        double k2 = __dadd_rn(__dadd_rn(__dmul_rn(kx, kx), __dmul_rn(ky, ky)), __dmul_rn(kz, kz));
+        if (i == mid) k2 = 1.0;
+        const double ck = -1.0 / k2;
+        // g = rho * (-1j / k2) with numpy's complex product
+        const double2 g = make_double2(-__dmul_rn(r.y, ck), __dmul_rn(r.x, ck));
+        double2 e0 = cscale(g, kx), e1 = cscale(g, ky), e2 = cscale(g, kz);
+        if (i == mid) e0 = e1 = e2 = make_double2(0.0, 0.0);
+        if (ex) {
+            ex[i] = e0;
+            ey[i] = e1;
+            ez[i] = e2;
+        }
+        en += e0.x * e0.x + e0.y * e0.y + e1.x * e1.x + e1.y * e1.y + e2.x * e2.x + e2.y * e2.y;
+    }
+    const double s = block_sum(en, scratch);
+    if (threadIdx.x == 0 && partials) partials[blockIdx.x] = s;
+}
+
+__global__ void finish_energy_kernel(const double *__restrict__ partials, int nblocks,
+                                     double half_L3, double *__restrict__ scalars) {
+    double s = 0.0;
+    for (int b = threadIdx.x; b < nblocks; b += 32) s += partials[b];
+    s = warp_sum(s);
+    if (threadIdx.x == 0) scalars[0] = half_L3 * s;
+}
+
+// (3) Hermitian guard: max |F[k] - conj F[-k]| over k in [1:,1:,1:] and max |F|
+__device__ __forceinline__ void atomic_max_nonneg(unsigned long long *a, double v) {
+    atomicMax(a, (unsigned long long)__double_as_longlong(v));
+}
+
+__global__ void mismatch_kernel(const double2 *__restrict__ ex, const double2 *__restrict__ ey,
+                                const double2 *__restrict__ ez, int N,
+                                unsigned long long *__restrict__ maxbits) {
+    const int64_t N3 = (int64_t)N * N * N;
+    double mm[3] = {0.0, 0.0, 0.0}, sc[3] = {0.0, 0.0, 0.0};
+    const double2 *F[3] = {ex, ey, ez};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N3;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int iz = (int)(i % N), iy = (int)((i / N) % N), ix = (int)(i / ((int64_t)N * N));
+        const bool paired = ix > 0 && iy > 0 && iz > 0;
+        const int64_t j = ((int64_t)(N - ix) * N + (N - iy)) * N + (N - iz);
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const double2 a = F[d][i];
+            sc[d] = fmax(sc[d], hypot(a.x, a.y));
+            if (paired) {
+                const double2 b = F[d][j];
+                mm[d] = fmax(mm[d], hypot(a.x - b.x, a.y + b.y));
+            }
+        }
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        double a = mm[d], b = sc[d];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+            b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomic_max_nonneg(maxbits + d, a);
+            atomic_max_nonneg(maxbits + 3 + d, b);
+        }
+    }
+}
+
+__global__ void finish_mismatch_kernel(const unsigned long long *__restrict__ maxbits,
+                                       double *__restrict__ scalars) {
+    double worst = 0.0;
+    for (int d = 0; d < 3; ++d) {
+        const double m = __longlong_as_double((long long)maxbits[d]);
+        const double s = __longlong_as_double((long long)maxbits[3 + d]);
+        if (s > 0.0) worst = fmax(worst, m / s);
+    }
+    scalars[1] = worst;
+}
+
+// (4) padded, shaped, deconvolved and Hermitian-symmetrised half spectra /n^3
+__global__ void pad_half_kernel(const double2 *__restrict__ ex, const double2 *__restrict__ ey,
+                                const double2 *__restrict__ ez, const double *__restrict__ shape,
+                                const double *__restrict__ deconv, double2 *__restrict__ spec,
+                                int N, int n, int64_t nhalf, double scale) {
+    const int nh1 = n / 2 + 1;
+    const double2 *F[3] = {ex, ey, ez};
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nhalf;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const int fz = (int)(j % nh1);
+        const int64_t t = j / nh1;
+        const int fy = (int)(t % n), fx = (int)(t / n);
+        const int px = band_index(fx, N, n), py = band_index(fy, N, n), pz = band_index(fz, N, n);
+        const int qx = band_index((n - fx) % n, N, n), qy = band_index((n - fy) % n, N, n),
+                  qz = band_index((n - fz) % n, N, n);
+        const bool hp = px >= 0 && py >= 0 && pz >= 0;
+        const bool hq = qx >= 0 && qy >= 0 && qz >= 0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            double2 y = make_double2(0.0, 0.0);
+            if (hp) {
+                double2 v = F[d][((int64_t)px * N + py) * N + pz];
+                v = cscale(cscale(cscale(v, shape[px]), shape[py]), shape[pz]);
+                v = cscale(cscale(cscale(v, deconv[px]), deconv[py]), deconv[pz]);
+                y.x += v.x;
+                y.y += v.y;
+            }
+            if (hq) {
+                double2 v = F[d][((int64_t)qx * N + qy) * N + qz];
+                v = cscale(cscale(cscale(v, shape[qx]), shape[qy]), shape[qz]);
+                v = cscale(cscale(cscale(v, deconv[qx]), deconv[qy]), deconv[qz]);
+                y.x += v.x;
+                y.y -= v.y;
+            }
+            spec[d * nhalf + j] = make_double2(0.5 * scale * y.x, 0.5 * scale * y.y);
+        }
+    }
+}
+
+__global__ void interleave_kernel(const double *__restrict__ f3, double4 *__restrict__ out,
+                                  int64_t n3) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n3;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = make_double4(f3[i], f3[n3 + i], f3[2 * n3 + i], 0.0);
+}
+
+// complex API helpers: full-spectrum truncate / pad
+__global__ void modes_from_full_kernel(const double2 *__restrict__ spec,
+                                       const double *__restrict__ deconv,
+                                       double2 *__restrict__ out, int N, int n, double inv_n3) {
+    const int64_t N3 = (int64_t)N * N * N;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N3;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int iz = (int)(i % N), iy = (int)((i / N) % N), ix = (int)(i / ((int64_t)N * N));
+        const int fx = pmod(ix - N / 2, n), fy = pmod(iy - N / 2, n), fz = pmod(iz - N / 2, n);
+        double2 v = spec[((int64_t)fx * n + fy) * n + fz];
+        v = cscale(v, deconv[ix]);
+        v = cscale(v, deconv[iy]);
+        v = cscale(v, deconv[iz]);
+        out[i] = cscale(v, inv_n3);
+    }
+}
+
+__global__ void pad_full_kernel(const double2 *__restrict__ modes,
+                                const double *__restrict__ deconv, double2 *__restrict__ grid,
+                                int N, int n, double scale) {
+    const int64_t n3 = (int64_t)n * n * n;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n3;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const int fz = (int)(j % n), fy = (int)((j / n) % n), fx = (int)(j / ((int64_t)n * n));
+        const int px = band_index(fx, N, n), py = band_index(fy, N, n), pz = band_index(fz, N, n);
+        double2 v = make_double2(0.0, 0.0);
+        if (px >= 0 && py >= 0 && pz >= 0) {
+            v = modes[((int64_t)px * N + py) * N + pz];
+            v = cscale(cscale(cscale(v, deconv[px]), deconv[py]), deconv[pz]);
+            v = make_double2(v.x * scale, v.y * scale);
+        }
+        grid[j] = v;
+    }
+}
+
+int blocks_for(int64_t work, int threads, int sm_count, int cap_per_sm = 16) {
+    int64_t b = (work + threads - 1) / threads;
+    const int64_t cap = (int64_t)sm_count * cap_per_sm;
+    if (b > cap) b = cap;
+    return (int)(b < 1 ? 1 : b);
+}
+
+int exec_z2d_fields(Plan &p, cudaStream_t s) {
+    cufftResult r = cufftSetStream(p.z2d3, s);
+    if (r != CUFFT_SUCCESS) return fail_cufft(r, "cufftSetStream(z2d)");
+    if (p.z2d_strided) {
+        r = cufftExecZ2D(p.z2d3, reinterpret_cast<cufftDoubleComplex *>(p.spec), p.field);
+        if (r != CUFFT_SUCCESS) return fail_cufft(r, "cufftExecZ2D");
+    } else {
+        r = cufftExecZ2D(p.z2d3, reinterpret_cast<cufftDoubleComplex *>(p.spec), p.field3);
+        if (r != CUFFT_SUCCESS) return fail_cufft(r, "cufftExecZ2D");
+        interleave_kernel<<<blocks_for(p.n3, 256, p.sm_count), 256, 0, s>>>(
+            p.field3, reinterpret_cast<double4 *>(p.field), p.n3);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return fail_cuda(e, "interleave_kernel");
+    }
+    p.field_valid = true;
+    return PIF_OK;
+}
+
+int guard_and_pad(Plan &p, const double2 *ex, const double2 *ey, const double2 *ez, int shape,
+                  double *scalars, cudaStream_t s) {
+    const int64_t N3 = (int64_t)p.N * p.N * p.N;
+    cudaError_t e = cudaMemsetAsync(p.maxbits, 0, sizeof(unsigned long long) * 6, s);
+    if (e != cudaSuccess) return fail_cuda(e, "zero max slots");
+    mismatch_kernel<<<blocks_for(N3, 256, p.sm_count), 256, 0, s>>>(ex, ey, ez, p.N, p.maxbits);
+    finish_mismatch_kernel<<<1, 1, 0, s>>>(p.maxbits, scalars);
+    const double *shp = p.shape_tab + (shape == PIF_SHAPE_CIC ? p.N : 0);
+    pad_half_kernel<<<blocks_for(p.nhalf, 256, p.sm_count), 256, 0, s>>>(
+        ex, ey, ez, shp, p.deconv, p.spec, p.N, p.n, p.nhalf, 1.0 / (double)p.n3);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return fail_cuda(e, "guard/pad kernels");
+    return exec_z2d_fields(p, s);
+}
+
+}  // namespace
+
+int launch_modes_from_spec(Plan &p, double *modes, cudaStream_t s) {
+    cufftResult r = cufftSetStream(p.d2z, s);
+    if (r != CUFFT_SUCCESS) return fail_cufft(r, "cufftSetStream(d2z)");
+    r = cufftExecD2Z(p.d2z, p.grid, reinterpret_cast<cufftDoubleComplex *>(p.spec));
+    if (r != CUFFT_SUCCESS) return fail_cufft(r, "cufftExecD2Z");
+    const int64_t N3 = (int64_t)p.N * p.N * p.N;
+    modes_from_spec_kernel<<<blocks_for(N3, 256, p.sm_count), 256, 0, s>>>(
+        p.spec, p.deconv, reinterpret_cast<double2 *>(modes), p.N, p.n, 1.0 / (double)p.n3);
+    return fail_cuda(cudaGetLastError(), "modes_from_spec_kernel");
+}
+
+int launch_solve_fields(Plan &p, const double *raw, int shape, double *rho_out, double *scalars,
+                        bool energy, const double *ex, const double *ey, const double *ez,
+                        cudaStream_t s) {
+    const int64_t N3 = (int64_t)p.N * p.N * p.N;
+    double2 *Ex = p.emodes, *Ey = p.emodes + N3, *Ez = p.emodes + 2 * N3;
+    if (raw) {
+        const int blocks = blocks_for(N3, 256, p.sm_count);
+        const double *shp = p.shape_tab + (shape == PIF_SHAPE_CIC ? p.N : 0);
+        poisson_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const double2 *>(raw), 1, shp,
+                                              p.inv_L3, p.kvec,
+                                              reinterpret_cast<double2 *>(rho_out), Ex, Ey, Ez,
+                                              p.partials, p.N);
+        if (energy) finish_energy_kernel<<<1, 32, 0, s>>>(p.partials, blocks, p.half_L3, scalars);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return fail_cuda(e, "poisson_kernel");
+    } else {
+        cudaError_t e = cudaMemcpyAsync(Ex, ex, sizeof(double2) * N3, cudaMemcpyDeviceToDevice, s);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(Ey, ey, sizeof(double2) * N3, cudaMemcpyDeviceToDevice, s);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(Ez, ez, sizeof(double2) * N3, cudaMemcpyDeviceToDevice, s);
+        if (e != cudaSuccess) return fail_cuda(e, "copy E modes");
+    }
+    return guard_and_pad(p, Ex, Ey, Ez, shape, scalars, s);
+}
+
+int launch_field_energy(Plan &p, const double *rho, double *scalars, cudaStream_t s) {
+    const int64_t N3 = (int64_t)p.N * p.N * p.N;
+    const int blocks = blocks_for(N3, 256, p.sm_count);
+    poisson_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const double2 *>(rho), 0, p.shape_tab,
+                                          p.inv_L3, p.kvec, nullptr, nullptr, nullptr, nullptr,
+                                          p.partials, p.N);
+    finish_energy_kernel<<<1, 32, 0, s>>>(p.partials, blocks, p.half_L3, scalars);
+    return fail_cuda(cudaGetLastError(), "field energy");
+}
+
+int launch_poisson(Plan &p, const double *rho, double *ex, double *ey, double *ez,
+                   cudaStream_t s) {
+    const int64_t N3 = (int64_t)p.N * p.N * p.N;
+    poisson_kernel<<<blocks_for(N3, 256, p.sm_count), 256, 0, s>>>(
+        reinterpret_cast<const double2 *>(rho), 0, p.shape_tab, p.inv_L3, p.kvec, nullptr,
+        reinterpret_cast<double2 *>(ex), reinterpret_cast<double2 *>(ey),
+        reinterpret_cast<double2 *>(ez), nullptr, p.N);
+    return fail_cuda(cudaGetLastError(), "poisson");
+}
+
+int launch_type1_complex_spread(Plan &p, const double *pts, const double *vals, int64_t M,
+                                cudaStream_t s);
+int launch_type2_complex_interp(Plan &p, const double *pts, int64_t M, double *out,
+                                cudaStream_t s);
+int ensure_complex(Plan &p);
+
+int launch_type1_complex(Plan &p, const double *pts, const double *vals, int64_t M,
+                         double *modes, cudaStream_t s) {
+    int rc = ensure_complex(p);
+    if (rc != PIF_OK) return rc;
+    rc = launch_type1_complex_spread(p, pts, vals, M, s);
+    if (rc != PIF_OK) return rc;
+    cufftResult r = cufftSetStream(p.z2z, s);
+    if (r == CUFFT_SUCCESS)
+        r = cufftExecZ2Z(p.z2z, reinterpret_cast<cufftDoubleComplex *>(p.cgrid),
+                         reinterpret_cast<cufftDoubleComplex *>(p.cgrid), CUFFT_FORWARD);
+    if (r != CUFFT_SUCCESS) return fail_cufft(r, "cufftExecZ2Z forward");
+    const int64_t N3 = (int64_t)p.N * p.N * p.N;
+    modes_from_full_kernel<<<blocks_for(N3, 256, p.sm_count), 256, 0, s>>>(
+        p.cgrid, p.deconv, reinterpret_cast<double2 *>(modes), p.N, p.n, 1.0 / (double)p.n3);
+    return fail_cuda(cudaGetLastError(), "modes_from_full_kernel");
+}
+
+int launch_type2_complex(Plan &p, const double *modes, const double *pts, int64_t M,
+                         double *out, cudaStream_t s) {
+    int rc = ensure_complex(p);
+    if (rc != PIF_OK) return rc;
+    pad_full_kernel<<<blocks_for(p.n3, 256, p.sm_count), 256, 0, s>>>(
+        reinterpret_cast<const double2 *>(modes), p.deconv, p.cgrid, p.N, p.n,
+        1.0 / (double)p.n3);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail_cuda(e, "pad_full_kernel");
+    cufftResult r = cufftSetStream(p.z2z, s);
+    if (r == CUFFT_SUCCESS)
+        r = cufftExecZ2Z(p.z2z, reinterpret_cast<cufftDoubleComplex *>(p.cgrid),
+                         reinterpret_cast<cufftDoubleComplex *>(p.cgrid), CUFFT_INVERSE);
+    if (r != CUFFT_SUCCESS) return fail_cufft(r, "cufftExecZ2Z inverse");
+    return launch_type2_complex_interp(p, pts, M, out, s);
+}
+
+}  // namespace pif

@@ -1,0 +1,119 @@
+// Internal declarations shared by the CUDA translation units of libpifb200.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/pif_b200.h"
+
+namespace pif {
+
+// Fused-kernel specialisations exist for stencil widths up to this value; wider
+// windows (eps < 1e-8) take the generic one-thread-per-particle path.
+constexpr int kMaxFastW = 8;
+constexpr int kMaxW = 17;          // eps >= 1e-16 (nufft.py:74)
+constexpr int kSub = 8;            // particles per warp sub-batch (fast kernels)
+constexpr int kWarpsPerBlock = 4;  // fast kernels: one work item per warp
+constexpr int kDiagSlots = 6;
+
+struct Plan {
+    int N = 0, n = 0, w = 0, device = 0;
+    double L = 0, eps = 0, beta = 0, h = 0, inv_L3 = 0, half_L3 = 0;
+    int64_t n3 = 0, nhalf = 0;     // n^3, n*n*(n/2+1)
+    int seg = 8;                   // cells per z-segment work item
+    double *deconv = nullptr;      // (N,)
+    double *kvec = nullptr;        // (N,) 2 pi m / L
+    double *grid = nullptr;        // n^3 real fine grid
+    double2 *spec = nullptr;       // 3 * nhalf complex: D2Z output / Z2D inputs
+    double *field = nullptr;       // n^3 * 4 interleaved E grid
+    double *field3 = nullptr;      // 3 * n^3 separate grids when strided C2R is unavailable
+    double2 *emodes = nullptr;     // 3 * N^3 complex: E modes (shape applied) for padding
+    double2 *cgrid = nullptr;      // n^3 complex grid (complex API, lazily allocated)
+    int32_t *cell_count = nullptr; // n^3 + 1
+    int32_t *cell_start = nullptr; // n^3 + 1
+    void *scan_tmp = nullptr;
+    size_t scan_tmp_bytes = 0;
+    unsigned int *work = nullptr;  // work counters for persistent kernels (4)
+    double *partials = nullptr;    // per-block diagnostic / reduction partials
+    int partial_blocks = 0;
+    unsigned long long *maxbits = nullptr;  // atomics for max reductions (8)
+    double *shape_tab = nullptr;   // (2, N): delta, cic shape factors
+    cufftHandle d2z = 0, z2d3 = 0, z2z = 0;
+    bool z2d_strided = false;      // Z2D writes the interleaved grid directly
+    bool field_valid = false;
+    int sm_count = 148;
+    int64_t bytes = 0;
+};
+
+void set_error(const std::string &msg);
+int fail_cuda(cudaError_t e, const char *where);
+int fail_cufft(cufftResult r, const char *where);
+
+// Kernel launchers (defined in the .cu files); all return PIF_* codes.
+int launch_wrap(Plan &p, double *x, double *y, double *z, int64_t M, cudaStream_t s);
+int launch_bin_keys(Plan &p, const pif_soa_t &src, int32_t *key, int32_t *rank, cudaStream_t s);
+int launch_bin_scatter(Plan &p, const pif_soa_t &src, pif_soa_t &dst, const int32_t *key,
+                       const int32_t *rank, bool vel, cudaStream_t s);
+int launch_spread(Plan &p, const pif_soa_t &sorted, const double *strengths, double q,
+                  cudaStream_t s);
+int launch_interp(Plan &p, pif_soa_t &sorted, bool push, double half, double dt,
+                  const double *tq, const double *sq, int has_b, int e_kind, int32_t *key,
+                  int32_t *rank, double *diag, double *E_out, cudaStream_t s);
+int launch_particle_diag(Plan &p, const pif_soa_t &ps, int e_kind, double *diag, cudaStream_t s);
+int launch_modes_from_spec(Plan &p, double *modes, cudaStream_t s);
+int launch_solve_fields(Plan &p, const double *raw, int shape, double *rho_out, double *scalars,
+                        bool energy, const double *ex, const double *ey, const double *ez,
+                        cudaStream_t s);
+int launch_field_energy(Plan &p, const double *rho, double *scalars, cudaStream_t s);
+int launch_poisson(Plan &p, const double *rho, double *ex, double *ey, double *ez,
+                   cudaStream_t s);
+int launch_type1_complex(Plan &p, const double *pts, const double *vals, int64_t M,
+                         double *modes, cudaStream_t s);
+int launch_type2_complex(Plan &p, const double *modes, const double *pts, int64_t M,
+                         double *out, cudaStream_t s);
+
+// ----------------------------------------------------------------------------
+// Device helpers
+// ----------------------------------------------------------------------------
+
+__host__ __device__ inline int pmod(int i, int n) {
+    int m = i % n;
+    return m < 0 ? m + n : m;
+}
+
+// First stencil index and scaled coordinate for one axis, in the reference's
+// arithmetic: c = x / h (true division), i0 = ceil(c - w/2) (_kernels.py:19,74).
+__device__ __forceinline__ double axis_coord(double x, double h) { return __ddiv_rn(x, h); }
+__device__ __forceinline__ double stencil_start(double c, int w) {
+    return ceil(__dsub_rn(c, 0.5 * w));
+}
+
+// Exponential-of-semicircle weight of grid point i0d + a for coordinate c:
+// t = (c - i) * 2/w, u = max(1 - t^2, 0), exp(beta (sqrt(u) - 1))
+// (_kernels.py:21-26), without FMA contraction so it rounds like the reference.
+__device__ __forceinline__ double es_weight(double c, double i, double inv_half, double beta) {
+    double t = __dmul_rn(__dsub_rn(c, i), inv_half);
+    double u = __dsub_rn(1.0, __dmul_rn(t, t));
+    u = u < 0.0 ? 0.0 : u;
+    return exp(__dmul_rn(beta, __dsub_rn(sqrt(u), 1.0)));
+}
+
+__device__ __forceinline__ double wrap_coord(double x, double L) {
+    // numpy float mod (sign follows the divisor) then the x == L guard
+    // (particles.py:65-70)
+    double r = fmod(x, L);
+    if (r != 0.0 && r < 0.0) r += L;
+    if (r >= L) r -= L;
+    return r;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+}  // namespace pif

@@ -1,0 +1,209 @@
+"""Device-resident particle-decomposition PIF stepper (one rank = one GPU).
+
+This is the B200 replacement of the reference's replicated-mode field operators
+and stepping loop (strategies.py:148-173 ``_PifFieldOps``, strategies.py:285-303
+``_stepping_loop``).  Per time step, all on one CUDA stream, nothing synchronises
+the host:
+
+    interp+push   fused type-2 gather + Boris push + wrap + next cell keys +
+                  diagnostic sums               (csrc/particles.cu, 1 launch)
+    bin           exclusive scan of cell counts + scatter into the other SoA
+                  buffer                         (CUB scan + 1 launch)
+    spread        binned register-tiled type-1 spreading   (1 launch)
+    modes         cuFFT D2Z + truncate/deconvolve -> allreduce buffer
+    allreduce     ONE collective per step of [raw rho_hat | diag(6)]
+                  (strategies.py:162-164 and the Recorder's :106 merged)
+    fields        finish_deposit + Poisson + energy + Hermitian guard + padded
+                  symmetrised half spectra + batched Z2D -> interleaved E grid
+    record        3 tiny device copies into the device-side record table
+
+The records come back to the host once, at the end of the run.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from ._device import is_torch, require_cuda
+from .diag import DeviceTimers
+from .particles import DeviceParticles
+
+
+class PifEngine:
+    """Owns the HBM state of one rank: SoA particles (double buffered), the
+    allreduce buffer and the device record table; the plan's native object owns
+    the fine grid, spectra, field grid and cell tables."""
+
+    def __init__(self, plan, count: int, device, *, q: float, m: float, externals, dt: float,
+                 shape: str = "delta", comm=None):
+        torch = require_cuda()
+        from .pif import boris_constants
+        if shape not in _native.SHAPE:
+            raise ValueError(f"unknown shape {shape!r}")
+        if dt <= 0:
+            raise ValueError(f"dt must be positive, got {dt}")
+        self.plan = plan
+        self.device = torch.device(device)
+        self.dp = plan.native(self.device)
+        self.handle = self.dp.handle
+        self.count = int(count)
+        self.parts = DeviceParticles(self.count, self.device)
+        N3 = plan.N ** 3
+        f64 = dict(dtype=torch.float64, device=self.device)
+        # allreduce buffer: raw type-1 modes (complex, interleaved) | diag sums | pad
+        self.red = torch.zeros(2 * N3 + 8, **f64)
+        self.raw = self.red[:2 * N3]
+        self.diag = self.red[2 * N3:2 * N3 + 6]
+        self.rho = torch.zeros((plan.N,) * 3, dtype=torch.complex128, device=self.device)
+        self.scalars = torch.zeros(4, **f64)
+        self.q, self.m, self.dt = float(q), float(m), float(dt)
+        half, tq, sq, has_b = boris_constants(self.q / self.m, self.dt, externals.B)
+        self.half = float(half)
+        self._tq, self._sq = _native.d3(tq), _native.d3(sq)
+        self.has_b = int(has_b)
+        self.e_kind = _native.EXT[externals.e_kind]
+        self.shape = _native.SHAPE[shape]
+        self.externals = externals
+        self.comm = comm
+        self.rec = None
+        self.dtimers = DeviceTimers(enabled=False)
+        self.launches = 0   # native kernel launches issued (for bench accounting)
+
+    # -- plumbing -------------------------------------------------------------
+    def _stream(self):
+        return _native.stream_handle(self.device)
+
+    def _soa(self, which="cur"):
+        p = self.parts
+        i = p.cur if which == "cur" else 1 - p.cur
+        return _native.soa_from_store(p.buf[i], p.ids[i], p.count)
+
+    @classmethod
+    def for_ensemble(cls, ens, plan, externals, dt, shape="delta", comm=None, device=None):
+        from ._device import default_device
+        dev = device if device is not None else default_device(ens.x)
+        eng = cls(plan, ens.count, dev, q=ens.q_per_particle, m=ens.m_per_particle,
+                  externals=externals, dt=dt, shape=shape, comm=comm)
+        eng.load(ens.x, ens.v, np.arange(ens.count, dtype=np.int64))
+        return eng
+
+    def load(self, x, v, ids):
+        """Upload an AoS ensemble and bin it into cell order."""
+        torch = require_cuda()
+        if not is_torch(x):
+            x = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64))
+            v = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64))
+        if not is_torch(ids):
+            ids = torch.from_numpy(np.ascontiguousarray(ids, dtype=np.int64))
+        self.parts.upload(x.to(self.device), v.to(self.device), ids.to(self.device))
+        if self.count:
+            s = self._stream()
+            cur = self._soa()
+            _native.call("pif_wrap_points", self.handle, cur.x, cur.y, cur.z, self.count, s)
+            _native.call("pif_bin_keys", self.handle, ctypes.byref(cur),
+                         self.parts.key.data_ptr(), self.parts.rank.data_ptr(), s)
+            self._scatter()
+
+    def _scatter(self):
+        src, dst = self._soa("cur"), self._soa("alt")
+        _native.call("pif_bin_scatter", self.handle, ctypes.byref(src), ctypes.byref(dst),
+                     self.parts.key.data_ptr(), self.parts.rank.data_ptr(), 1, self._stream())
+        self.parts.swap()
+        self.launches += 2
+
+    # -- stages -----------------------------------------------------------------
+    def particle_diag(self):
+        cur = self._soa()
+        _native.call("pif_particle_diag", self.handle, ctypes.byref(cur), self.e_kind,
+                     self.diag.data_ptr(), self._stream())
+        self.launches += 2
+
+    def deposit(self):
+        """Scatter: binned spreading + D2Z + truncate/deconvolve -> raw modes."""
+        cur = self._soa()
+        s = self._stream()
+        _native.call("pif_spread_sorted", self.handle, ctypes.byref(cur), None, self.q, s)
+        _native.call("pif_grid_to_modes", self.handle, self.raw.data_ptr(), s)
+        self.launches += 3
+
+    def allreduce(self):
+        if self.comm is not None:
+            self.comm.allreduce_sum(self.red)
+
+    def solve_fields(self):
+        """finish_deposit + Poisson + energy + guard + padded spectra + Z2D."""
+        _native.call("pif_solve_fields", self.handle, self.raw.data_ptr(), self.shape,
+                     self.rho.data_ptr(), self.scalars.data_ptr(), self._stream())
+        self.launches += 6
+
+    def gather_push(self):
+        """Fused gather + Boris push, then bin the new positions."""
+        cur = self._soa()
+        _native.call("pif_interp_push", self.handle, ctypes.byref(cur), self.half, self.dt,
+                     self._tq, self._sq, self.has_b, self.e_kind, self.parts.key.data_ptr(),
+                     self.parts.rank.data_ptr(), self.diag.data_ptr(), self._stream())
+        self.launches += 2
+        if self.count:
+            self._scatter()
+
+    def record(self, slot: int):
+        r = self.rec[slot]
+        r[0:1].copy_(self.scalars[0:1])
+        r[1:6].copy_(self.diag[0:5])
+        r[6:7].copy_(self.scalars[1:2])
+
+    # -- whole runs -----------------------------------------------------------------
+    def run(self, steps: int, *, timers=None):
+        """Prime solve + record(0), then `steps` x (gather/push, solve, record)
+        (strategies.py:285-303).  Returns the device record table (steps+1, 8):
+        [W, sum v.v, sum vx, sum vy, sum vz, sum phi_ext, guard, 0]."""
+        torch = require_cuda()
+        self.rec = torch.zeros((steps + 1, 8), dtype=torch.float64, device=self.device)
+        dt = self.dtimers
+        dt.enabled = timers is not None
+        self.particle_diag()
+        self._solve(dt)
+        self.record(0)
+        for i in range(steps):
+            with dt.section("Gather"):
+                self.gather_push()
+            self._solve(dt)
+            self.record(i + 1)
+        if timers is not None:
+            dt.flush(timers)
+        return self.rec
+
+    def _solve(self, dt):
+        with dt.section("Scatter"):
+            self.deposit()
+        if self.comm is not None:
+            with dt.section("Allreduce"):
+                self.allreduce()
+        with dt.section("Gather"):
+            self.solve_fields()
+
+    def step_once(self):
+        """One full PD step (used by the bench loop and CUDA-graph capture)."""
+        self.gather_push()
+        self.deposit()
+        self.allreduce()
+        self.solve_fields()
+
+    def store_into(self, ens):
+        """Copy the particles back into an AoS ensemble, original order."""
+        x, v, _ = self.parts.download(sort_by_id=True)
+        if is_torch(ens.x):
+            ens.x = x.to(ens.x.device)
+            ens.v = v.to(ens.v.device)
+        else:
+            ens.x = x.cpu().numpy()
+            ens.v = v.cpu().numpy()
+        return ens
+
+    def rho_field(self):
+        from .spectral import FourierField
+        f = FourierField(self.plan.N, self.plan.L, self.rho.clone(), "charge-density")
+        return f

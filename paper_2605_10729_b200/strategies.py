@@ -1,0 +1,145 @@
+"""Serial and particle-decomposition runners (the north-star path).
+
+Same entry points and return contract as the reference's strategies module
+(/root/reference/pkg/src/pifsim/strategies.py:310-346): particles split into
+contiguous id slices (bench.py:184-188), modes replicated on every rank, one
+allreduce per step, per-step ``StepRecord`` diagnostics on the root rank.  The
+whole step runs on the rank's GPU through ``engine.PifEngine``; the only host
+work per run is sampling the initial ensemble and reading the records back.
+
+Domain decomposition and the space-time (parareal) strategy are out of scope
+for this tier: their runners exist for API compatibility and raise.
+"""
+
+from __future__ import annotations
+
+import time as _time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import nufft
+from ._device import require_cuda
+from .comm import Comm, RankContext
+from .diag import StepRecord, Timers
+from .engine import PifEngine
+from .samplers import BenchmarkSpec, id_slice, sample_benchmark
+
+
+@dataclass(frozen=True)
+class RunSetup:
+    """Resolved numerical configuration for one run (strategies.py:41-48)."""
+
+    spec: BenchmarkSpec
+    eps: float = 1e-7
+    shape: str = "delta"
+    diag_every: int = 1
+
+
+@dataclass(frozen=True)
+class CoarseSpec:
+    kind: str = "pif"
+    eps: float = 1e-3
+    n_c: int | None = None
+    dt: float | None = None
+
+    def __post_init__(self):
+        if self.kind not in ("pif", "pic"):
+            raise ValueError(f"coarse kind must be pif|pic, got {self.kind!r}")
+
+
+@dataclass(frozen=True)
+class PararealConfig:
+    ranks_time: int
+    tol: float = 1e-8
+    max_iters: int = 50
+    coarse: CoarseSpec = field(default_factory=CoarseSpec)
+    blocks: int = 1
+    record_states: bool = False
+    exact_iters: int | None = None
+
+
+def records_from_table(table: np.ndarray, *, steps: int, dt: float, q: float, m: float,
+                       total_charge: float, diag_every: int = 1):
+    """Turn the device record table [W, sum v.v, sum v, sum phi, guard] into
+    StepRecords exactly as Recorder.record composes them (strategies.py:96-117,
+    pif.py:60-68, 240-245)."""
+    every = max(1, diag_every)
+    out = []
+    for step in range(steps + 1):
+        if step != 0 and step % every != 0:
+            continue
+        W, svv, sx, sy, sz, sphi = (float(a) for a in table[step, :6])
+        ke = 0.5 * m * svv
+        u_ext = q * sphi
+        out.append(StepRecord(step=step, t=step * dt if step else 0.0, field_energy=W,
+                              kinetic_energy=ke, total_energy=W + ke + u_ext, px=m * sx,
+                              py=m * sy, pz=m * sz, total_charge=total_charge))
+    return out
+
+
+def _run_replicated(setup: RunSetup, comm: Comm | None, timers: Timers, device=None) -> dict:
+    torch = require_cuda()
+    spec = setup.spec
+    plan = nufft.make_plan(spec.N, spec.L, setup.eps)
+    externals = spec.externals()
+    size = comm.size if comm is not None else 1
+    rank = comm.rank if comm is not None else 0
+    lo, hi = id_slice(spec.num_particles, rank, size)
+    ens = sample_benchmark(spec, spec.seed, (lo, hi))
+    dev = torch.device(device) if device is not None else torch.device(
+        "cuda", torch.cuda.current_device())
+    with torch.cuda.device(dev):
+        eng = PifEngine(plan, ens.count, dev, q=ens.q_per_particle, m=ens.m_per_particle,
+                        externals=externals, dt=spec.dt, shape=setup.shape, comm=comm)
+        eng.load(ens.x, ens.v, ens.ids)
+        torch.cuda.synchronize(dev)
+        start = _time.perf_counter()
+        table = eng.run(spec.steps, timers=timers)
+        host = table.cpu().numpy()
+        loop_seconds = _time.perf_counter() - start
+    guard = float(host[:, 6].max()) if host.size else 0.0
+    if guard > 1e-10:
+        from .pif import FieldSymmetryError
+        raise FieldSymmetryError(f"field modes lost Hermitian symmetry (relative mismatch "
+                                 f"{guard:.3e})")
+    recs = records_from_table(host, steps=spec.steps, dt=spec.dt, q=ens.q_per_particle,
+                              m=ens.m_per_particle, total_charge=spec.Q_e,
+                              diag_every=setup.diag_every)
+    initial, records = recs[0], recs[1:]
+    # the reference's Recorder stamps t = (i+1)*dt for step i+1 (strategies.py:301)
+    for r in records:
+        r.t = r.step * spec.dt
+    return {
+        "records": records if rank == 0 else None,
+        "initial": initial,
+        "loop_seconds": loop_seconds,
+        "steps": spec.steps,
+        "timers": timers,
+        "engine": eng,
+    }
+
+
+def run_serial(setup: RunSetup, ctx: RankContext, timers: Timers | None = None) -> dict:
+    """Plain single-rank stepping (strategies.py:335-339): no communication."""
+    if ctx.world_size != 1:
+        raise ValueError("serial strategy runs on exactly one rank")
+    return _run_replicated(setup, None, timers or Timers(), ctx.device)
+
+
+def run_particle_decomposition(setup: RunSetup, ctx: RankContext,
+                               timers: Timers | None = None) -> dict:
+    """Particles split by id, modes replicated, allreduce-only communication
+    (strategies.py:342-346)."""
+    ctx.space = ctx.world
+    return _run_replicated(setup, ctx.world, timers or Timers(), ctx.device)
+
+
+def run_domain_decomposition(setup: RunSetup, ctx: RankContext, timers=None) -> dict:
+    raise NotImplementedError("domain decomposition (strategies.py:394-434) is outside this "
+                              "B200 particle-decomposition build")
+
+
+def run_parareal(setup: RunSetup, pcfg: PararealConfig, ctx: RankContext, timers=None) -> dict:
+    raise NotImplementedError("space-time parareal (strategies.py:507-686) is outside this "
+                              "B200 particle-decomposition build")
