@@ -1,0 +1,428 @@
+#!/usr/bin/env python
+"""bench.py — particle-decomposition PIF time step on B200 (one JSON line).
+
+Default workload (BASELINE.json configs[1], the metric's config): 3D-3V Landau
+damping, 64^3 modes, 2^27 particles per GPU (ppm 512), eps 1e-7 (w = 8),
+dt 0.003125, fp64.  A "step" is one full PD-PIF step: fused gather+push,
+binning, spreading, D2Z + truncate, ONE allreduce of [rho_hat | diag] (N > 1),
+field solve + 3x Z2D.  N GPUs run as torchrun ranks over NCCL; per-GPU work is
+fixed (weak scaling: N = 8 is the north-star 2^30-particle run) unless
+--scaling strong.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+--impl reference times the reference algorithm's CPU implementation (the C +
+numpy oracle port in oracle/, all host cores) on a bounded sample of the same
+workload; under torchrun only rank 0 runs it.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle-steps/sec (Landau 3D-3V, 64^3 modes) at 1/2/4/8 B200; % roofline"
+UNIT = "particle-steps/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--kind", default="landau", choices=["landau", "penning"])
+    ap.add_argument("--N", type=int, default=64)
+    ap.add_argument("--ppm", type=int, default=512, help="particles per mode (per GPU if weak)")
+    ap.add_argument("--eps", type=float, default=1e-7)
+    ap.add_argument("--dt", type=float, default=0.003125)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--cpu-particles", type=int, default=1 << 20)
+    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def workload_config(a, world):
+    from paper_2605_10729_b200.nufft import make_plan
+    w = make_plan(a.N, 1.0, a.eps).window.w
+    per_gpu = a.ppm * a.N ** 3 if a.scaling == "weak" else (a.ppm * a.N ** 3) // world
+    glob = per_gpu * world if a.scaling == "weak" else a.ppm * a.N ** 3
+    name = "Landau damping" if a.kind == "landau" else "Penning trap"
+    return {
+        "workload": f"3D-3V {name}, {a.N}^3 modes, {glob} particles "
+                    f"({per_gpu}/GPU), eps {a.eps:g} (w={w}), dt {a.dt:g}, fp64, "
+                    f"particle decomposition",
+        "modes_per_dim": a.N, "fine_grid": 2 * a.N, "window_w": w, "eps": a.eps, "dt": a.dt,
+        "particles_per_gpu": per_gpu, "global_particles": glob, "parallelism": f"pd{world}",
+        "l2": "particle SoA (48 B/particle) >> 126 MB L2: inputs larger than L2, no flush",
+    }, w, per_gpu, glob
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.index)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:6]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline / reference arm (oracle port of the reference algorithm)
+# ---------------------------------------------------------------------------
+
+def cpu_reference_run(a, particles: int, steps: int, warmup: int):
+    """Oracle PD on all host cores: returns (particle-steps/s, cores, sample text)."""
+    import numpy as np  # noqa: F401
+    from oracle import pif_oracle as o
+    from paper_2605_10729_b200.samplers import landau_spec, penning_spec, sample_benchmark
+    cores = os.cpu_count() or 1
+    ppm = max(1, particles // a.N ** 3)
+    mk = landau_spec if a.kind == "landau" else penning_spec
+    spec = mk(N=a.N, ppm=ppm, dt=a.dt, seed=0)
+    ens = sample_benchmark(spec, 0)
+    plan = o.make_plan(a.N, spec.L, a.eps)
+    run = o.PDRun(plan, ens.x, ens.v, ens.q_per_particle, ens.m_per_particle, L=spec.L,
+                  B=spec.B_ext, e_kind=spec.e_kind, dt=a.dt, ranks=cores)
+    for _ in range(warmup):
+        run.step()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        run.step()
+    dt = time.perf_counter() - t0
+    M = ens.count
+    sample = (f"{M} particles ({ppm}/mode) of the same {a.N}^3 workload, {steps} PD steps on "
+              f"{cores} host threads (oracle port: C window kernels + numpy pocketfft)")
+    return M * steps / dt, cores, sample, dt / steps
+
+
+def run_reference(a):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cfg, w, per_gpu, glob = workload_config(a, world)
+    steps = max(1, min(a.steps, 4))
+    val, cores, sample, sec = cpu_reference_run(a, a.cpu_particles, steps, min(a.warmup, 1))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
+        "steps": steps, "warmup": min(a.warmup, 1), "ms_per_step": sec * 1e3,
+        "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference samplers, seed 0)", "config": cfg,
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+
+def fp64_peak_tflops(torch, dev) -> float:
+    from paper_2605_10729_b200 import _native
+    lib = _native.load()
+    scratch = torch.zeros(8, dtype=torch.float64, device=dev)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    best = 0.0
+    flops = (_native.ctypes.c_double * 3)()
+    s = _native.stream_handle(dev)
+    for _ in range(6):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        _native.check(lib.pif_probe_fp64(scratch.data_ptr(), sms * 8, 256, 4096, s, flops))
+        b.record()
+        b.synchronize()
+        best = max(best, flops[0] / (a.elapsed_time(b) * 1e-3) / 1e12)
+    return best
+
+
+def load_ncu_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def run_b200(a):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_10729_b200 as pb
+    from paper_2605_10729_b200.comm import Comm, TorchDistTransport
+    from paper_2605_10729_b200.engine import PifEngine
+    from paper_2605_10729_b200.samplers import id_slice, sample_device
+
+    rank, world, local = dist_env()
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else torch.cuda.current_device())
+    torch.cuda.set_device(dev)
+    cfg, w, per_gpu, glob = workload_config(a, world)
+    mk = pb.landau_spec if a.kind == "landau" else pb.penning_spec
+    gspec = mk(N=a.N, ppm=max(1, glob // a.N ** 3), dt=a.dt, seed=0)
+    plan = pb.make_plan(a.N, gspec.L, a.eps)
+    comm = Comm(TorchDistTransport(), rank) if world > 1 else None
+    lo, hi = id_slice(glob, rank, world)
+    q = gspec.Q_e / glob
+    m = abs(gspec.Q_e) / glob
+    eng = PifEngine(plan, hi - lo, dev, q=q, m=m, externals=gspec.externals(), dt=a.dt,
+                    comm=comm)
+    x, v, ids = sample_device(gspec, (lo, hi), dev)
+    eng.load(x, v, ids)
+    del x, v, ids
+    torch.cuda.empty_cache()
+
+    peak = fp64_peak_tflops(torch, dev)
+
+    # prime solve (strategies.py:290) + warm-up steps
+    eng.particle_diag()
+    eng.deposit()
+    eng.allreduce()
+    eng.solve_fields()
+    for _ in range(a.warmup):
+        eng.step_once()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+
+    K = a.steps
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    t_int = [(ev(), ev()) for _ in range(K)]
+    t_spr = [(ev(), ev()) for _ in range(K)]
+    t_bin = [(ev(), ev()) for _ in range(K)]
+    t_fld = [(ev(), ev()) for _ in range(K)]
+    t_red = [(ev(), ev()) for _ in range(K)]
+    start, stop = ev(), ev()
+    clocks = ClockSampler(dev.index)
+    if rank == 0:
+        clocks.start()
+        time.sleep(0.3)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    launches0 = eng.launches
+    start.record()
+    for i in range(K):
+        t_int[i][0].record()
+        eng.interp_push()
+        t_int[i][1].record()
+        t_bin[i][0].record()
+        eng.rebin()
+        t_bin[i][1].record()
+        t_spr[i][0].record()
+        eng.spread()
+        t_spr[i][1].record()
+        eng.modes()
+        t_red[i][0].record()
+        eng.allreduce()
+        t_red[i][1].record()
+        t_fld[i][0].record()
+        eng.solve_fields()
+        t_fld[i][1].record()
+    stop.record()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop() if rank == 0 else None
+    launches = eng.launches - launches0
+    T = start.elapsed_time(stop) * 1e-3
+    if world > 1:
+        tt = torch.tensor([T], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        T = float(tt[0])
+    avg = lambda ts: sum(a_.elapsed_time(b_) for a_, b_ in ts) / len(ts) * 1e-3  # noqa: E731
+    s_int, s_spr, s_bin, s_fld, s_red = avg(t_int), avg(t_spr), avg(t_bin), avg(t_fld), avg(t_red)
+    value = glob * K / T
+    f_interp = 6 * w ** 3 + w ** 2
+    f_spread = 2 * w ** 3 + w ** 2
+    f_step = 8 * w ** 3 + 2 * w ** 2
+    achieved = per_gpu * f_interp / s_int / 1e12
+    traffic = load_ncu_traffic()
+    tr = traffic.get(f"interp_w{w}_ppg{per_gpu}")
+    roofline = {
+        "bound": "fp64", "kernel": "interp_fast_kernel<8,true> (fused gather + Boris push)",
+        "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+        "traffic": tr,
+        "peak_source": "FP64 DFMA probe measured live in this run (MEASURED_PEAKS.json has no "
+                       "FP64 figure); HBM peak from MEASURED_PEAKS.json",
+        "algorithmic_flops_per_particle": {"interp": f_interp, "spread": f_spread,
+                                           "step": f_step},
+        "spread": {"achieved": per_gpu * f_spread / s_spr / 1e12,
+                   "frac": per_gpu * f_spread / s_spr / 1e12 / peak},
+        "step_fp64_frac": (per_gpu * f_step / (T / K) / 1e12) / peak,
+        "hbm_frac_step": None,
+        "stage_ms": {"interp_push": s_int * 1e3, "bin": s_bin * 1e3, "spread": s_spr * 1e3,
+                     "fields": s_fld * 1e3, "allreduce": s_red * 1e3},
+    }
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            hbm = float(json.load(f)["hbm_gbs"])
+        roofline["hbm_frac_step"] = per_gpu * 120 / (T / K) / 1e9 / hbm
+    except (OSError, KeyError, ValueError):
+        pass
+
+    # end to end through the public API with host buffers
+    e2e = None
+    if not a.no_e2e:
+        e2e = run_e2e(a, eng, torch, dist, world, per_gpu, glob, dev)
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        val, cores, sample, _ = cpu_reference_run(a, a.cpu_particles, a.cpu_steps, 0)
+        cpu = {"value": val, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": a.warmup, "ms_per_step": T / K * 1e3, "higher_is_better": True,
+            "scaling": a.scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (device sampler: Landau inverse-CDF / Penning Gaussian, "
+                    "N(0,1) velocities)",
+            "config": cfg, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(a, eng, torch, dist, world, per_gpu, glob, dev):
+    """pif_step-style use with host (pinned) particle arrays: per step H2D of
+    x, v, upload + wrap + bin, spread, D2Z, allreduce, fields, gather+push,
+    D2H of x, v, ids (cell order) and the field energy."""
+    M = eng.count
+    xh = torch.empty((M, 3), dtype=torch.float64, pin_memory=True)
+    vh = torch.empty((M, 3), dtype=torch.float64, pin_memory=True)
+    idh = torch.empty(M, dtype=torch.int64, pin_memory=True)
+    x, v, ids = eng.parts.download(sort_by_id=False)
+    xh.copy_(x)
+    vh.copy_(v)
+    idh.copy_(ids)
+    del x, v, ids
+    # the host arrays hold the state: D2H writes back into them, the next step
+    # uploads them again (pif_step on numpy arrays)
+    xo, vo, io = xh, vh, idh
+    wo = torch.empty(1, dtype=torch.float64, pin_memory=True)
+    xd = torch.empty((M, 3), dtype=torch.float64, device=dev)
+    vd = torch.empty((M, 3), dtype=torch.float64, device=dev)
+    idd = torch.empty(M, dtype=torch.int64, device=dev)
+
+    def one():
+        xd.copy_(xh, non_blocking=True)
+        vd.copy_(vh, non_blocking=True)
+        idd.copy_(idh, non_blocking=True)
+        eng.load(xd, vd, idd)
+        eng.deposit()
+        eng.allreduce()
+        eng.solve_fields()
+        eng.gather_push()
+        soa = eng.parts.soa[:, :M]
+        xo.copy_(soa[0:3].t(), non_blocking=True)
+        vo.copy_(soa[3:6].t(), non_blocking=True)
+        io.copy_(eng.parts.ids[eng.parts.cur][:M], non_blocking=True)
+        wo.copy_(eng.scalars[0:1], non_blocking=True)
+
+    one()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    K = max(1, a.e2e_steps)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(K):
+        one()
+    e.record()
+    torch.cuda.synchronize(dev)
+    T = s.elapsed_time(e) * 1e-3
+    if world > 1:
+        tt = torch.tensor([T], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        T = float(tt[0])
+    return {"value": glob * K / T, "unit": UNIT, "h2d_bytes_per_step": M * (48 + 8) * world,
+            "d2h_bytes_per_step": (M * (48 + 8) + 8) * world, "steps": K,
+            "api": "PifEngine.load (host pinned x,v,ids) -> deposit -> allreduce -> "
+                   "solve_fields -> gather_push -> D2H x,v,ids + W"}
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_b200(a)
+
+
+if __name__ == "__main__":
+    main()

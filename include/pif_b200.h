@@ -148,6 +148,13 @@ int pif_type1_complex(pif_plan_t plan, const double *pts, const double *vals, in
 int pif_type2_complex(pif_plan_t plan, const double *modes, const double *pts, int64_t M,
                       double *out, void *stream);
 
+/* ---- measurement ------------------------------------------------------------
+ * FP64 DFMA throughput probe (the roofline denominator; MEASURED_PEAKS.json has
+ * no FP64 figure).  Launches blocks x threads threads, each running `iters`
+ * iterations of 8 independent FMAs; *flops_out = flops issued. */
+int pif_probe_fp64(double *scratch, int blocks, int threads, int iters, void *stream,
+                   double *flops_out);
+
 #ifdef __cplusplus
 }
 #endif

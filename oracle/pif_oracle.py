@@ -455,3 +455,55 @@ def run_pd(plan: Plan, x: np.ndarray, v: np.ndarray, q: float, m: float, *, L: f
         records.append(record(i + 1, (i + 1) * dt, rho))
     out.update(records=records, initial=initial, x=np.concatenate(xs), v=np.concatenate(vs))
     return out
+
+
+class PDRun:
+    """Stateful oracle PD stepper for timing (bench.py cpu_baseline and
+    --impl reference): `ranks` id slices on `ranks` threads, like the
+    reference's spawn_spmd PD run (strategies.py:285-303)."""
+
+    def __init__(self, plan: Plan, x, v, q, m, *, L, B=(0.0, 0.0, 0.0), e_kind="none", dt,
+                 ranks=1, shape="delta"):
+        self.plan, self.q, self.m, self.L, self.B = plan, q, m, L, B
+        self.e_kind, self.dt, self.ranks, self.shape = e_kind, dt, ranks, shape
+        M = x.shape[0]
+        base, extra = divmod(M, ranks)
+        self.xs, self.vs = [], []
+        for r in range(ranks):
+            lo = r * base + min(r, extra)
+            hi = lo + base + (1 if r < extra else 0)
+            self.xs.append(np.ascontiguousarray(x[lo:hi]))
+            self.vs.append(np.ascontiguousarray(v[lo:hi]))
+        self.rho = self._solve()
+
+    def _par(self, fn):
+        out = [None] * self.ranks
+        ts = [threading.Thread(target=lambda r=r: out.__setitem__(r, fn(r)))
+              for r in range(self.ranks)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        return out
+
+    def _solve(self):
+        raws = self._par(lambda r: type1(self.plan, self.xs[r],
+                                         np.full(self.xs[r].shape[0], self.q)))
+        return finish_deposit(tree_sum(raws), self.plan, self.shape)
+
+    def step(self):
+        plan = self.plan
+        E = poisson_efield(self.rho, self.L)
+        s = shape_factors(plan.N, self.shape)
+        comps = []
+        for f in E:
+            c = f.copy()
+            apply_shape(c, s)
+            comps.append(c)
+        grids = field_grids(plan, comps)
+        E_at = self._par(lambda r: interp3(plan, grids, prep_points(self.xs[r], self.L)))
+        for r in range(self.ranks):
+            self.xs[r], self.vs[r] = boris_push(self.xs[r], self.vs[r], E_at[r], self.q, self.m,
+                                                self.B, self.e_kind, self.dt, self.L)
+        self.rho = self._solve()
+        return field_energy(poisson_efield(self.rho, self.L), self.L)

@@ -1,0 +1,65 @@
+// Fast fp64 exponential-of-semicircle weight for the sm_100a kernels.
+//
+// phi(t) = exp(beta (sqrt(1 - t^2) - 1)) (_kernels.py:21-26) with
+//  * sqrt from the MUFU.RSQ64H seed + two Newton corrections (full fp64), and
+//  * exp by Cody-Waite reduction onto a 32-entry 2^(j/32) table in shared memory
+//    plus a degree-6 polynomial (|r| <= ln2/64, truncation < 4e-18).
+// About 24 FP64-pipe instructions per weight instead of ~42 for libdevice
+// exp()+sqrt(); agreement with the reference formula is ~1e-15 relative
+// (tools/dmma_probe.cu measures it on the GPU).
+#pragma once
+
+namespace pif {
+
+__device__ __constant__ static const double kExp2Table[32] = {
+    1.0, 1.0218971486541166, 1.0442737824274138, 1.0671404006768237, 1.0905077326652577,
+    1.1143867425958924, 1.1387886347566916, 1.1637248587775775, 1.189207115002721,
+    1.215247359980469, 1.241857812073484, 1.2690509571917332, 1.2968395546510096,
+    1.3252366431597413, 1.3542555469368927, 1.383909881963832, 1.4142135623730951,
+    1.4451808069770467, 1.4768261459394993, 1.5091644275934228, 1.5422108254079407,
+    1.5759808451078865, 1.6104903319492543, 1.645755478153965, 1.681792830507429,
+    1.718619298122478, 1.7562521603732995, 1.7947090750031072, 1.8340080864093424,
+    1.8741676341103, 1.9152065613971474, 1.9571441241754002};
+
+// e^y for y in [-40, 0]; tab = kExp2Table staged in shared memory
+__device__ __forceinline__ double exp_neg_fast(double y, const double *tab) {
+    const double magic = 6755399441055744.0;  // 1.5 * 2^52
+    double kd = fma(y, 46.16624130844683, magic);  // 32/ln2
+    const int k = __double2loint(kd);
+    kd -= magic;
+    double r = fma(kd, -0.021660849392475257, y);  // ln2/32 (hi, 40 bits)
+    r = fma(kd, -2.303438301614937e-14, r);        // ln2/32 (lo)
+    double p = 1.0 / 720.0;
+    p = fma(p, r, 1.0 / 120.0);
+    p = fma(p, r, 1.0 / 24.0);
+    p = fma(p, r, 1.0 / 6.0);
+    p = fma(p, r, 0.5);
+    p = fma(p, r, 1.0);
+    p = fma(p, r, 1.0);
+    double v = tab[k & 31] * p;
+    return __hiloint2double(__double2hiint(v) + ((k >> 5) << 20), __double2loint(v));
+}
+
+__device__ __forceinline__ double rsqrt_seed(double u) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(u));
+    return y;
+}
+
+// sqrt(u) for u in [1e-300, 1]: seed + Newton on 1/sqrt + one sqrt correction
+__device__ __forceinline__ double sqrt_fast(double u) {
+    double y = rsqrt_seed(u);
+    double e = fma(-u * y, y, 1.0);
+    y = fma(0.5 * y, e, y);
+    double s = u * y;
+    return fma(0.5 * y, fma(-s, s, u), s);
+}
+
+__device__ __forceinline__ double es_weight_fast(double c, double i, double inv_half, double beta,
+                                                 const double *tab) {
+    const double t = __dmul_rn(__dsub_rn(c, i), inv_half);
+    const double u = fmax(fma(-t, t, 1.0), 1e-300);
+    return exp_neg_fast(fma(beta, sqrt_fast(u), -beta), tab);
+}
+
+}  // namespace pif

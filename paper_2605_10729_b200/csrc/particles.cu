@@ -5,16 +5,17 @@
 //   _kernels.py:125-183, and pif.boris_push, pif.py:140-158),
 //   diagnostics sums (strategies.py:96-106), generic wide-window fallbacks.
 //
-// Fast kernels (w <= 8): one warp owns a work item = a z-segment of one
-// (i0x, i0y) column of stencil cells.  All particles of a cell share one
-// w x w x w footprint, so a lane keeps its footprint points in registers:
-// lane owns (a,b) pairs q = lane and lane+32 of the w*w xy-footprint, times w
-// z planes.  Moving to the next cell along z rotates the register planes by
-// one (a register move, no reload of the other w-1 planes), so per cell only
-// one new plane is flushed (spread, REDG.ADD.F64) or loaded (gather).
+// Fast kernels (w <= 8): particles are binned by their ES-stencil start cell
+// (i0x, i0y, i0z), so every particle of a cell shares one w^3 footprint.  One
+// warp owns a work item = a z-segment of one (i0x, i0y) column of cells and
+// keeps the 8 x 8 x 8 footprint block in DMMA (fp64 mma.sync m8n8k4) fragments:
+// spreading accumulates it, gathering contracts it; the z-slot of a plane is
+// its index mod 8, so stepping to the next cell in z flushes (spread) or loads
+// (gather) exactly one plane.  Window weights come from es_fast.cuh.
 #include <cub/cub.cuh>
 
 #include "pif_internal.cuh"
+#include "es_fast.cuh"
 
 namespace pif {
 
@@ -78,77 +79,135 @@ __global__ void bin_scatter_kernel(pif_soa_t src, pif_soa_t dst, const int32_t *
 }
 
 // ----------------------------------------------------------------------------
-// shared per-warp staging of one sub-batch (<= kSub particles of one cell)
+// DMMA building blocks
 // ----------------------------------------------------------------------------
 
-template <int W>
-struct WarpStage {
-    double wt[kSub][3][W];   // window weights; x row optionally scaled by strength
-    double c[kSub][3];       // coordinates in grid units
-    double i0[kSub][3];      // stencil starts
+// D(8x8) += A(8x4) B(4x8), fp64 tensor-core MMA (SASS DMMA.8x8x4).  Fragments:
+// A[row = lane>>2][col = lane&3], B[row = lane&3][col = lane>>2],
+// D[row = lane>>2][col = 2*(lane&3) + {0,1}] (checked by tools/dmma_probe.cu).
+__device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// Per-warp staging of one chunk of up to kChunk consecutive (cell-sorted)
+// particles of a work item; chunks run across cell boundaries.  Weights are
+// padded to 8 with zeros (rows a >= w are never written), laid out for the
+// fragment loads.
+constexpr int kChunk = 32;
+
+struct WarpChunk {
+    double wx[8][kChunk];   // [a][p]  x weights (spreading: times the strength)
+    double wy[8][kChunk];   // [b][p]
+    double wz[kChunk][8];   // [p][c]
+    double c[3][kChunk];    // coordinates in grid units
+    double i0[3][kChunk];   // stencil starts
+    double x[3][kChunk];    // positions (gather+push)
+    double E[3][kChunk];    // gathered field (gather+push)
 };
 
-// Phase 1: coordinates + stencil starts (24 lanes, one (particle, axis) each).
-// Phase 2: 3*W*kSub weights spread over the 32 lanes.
+__device__ __forceinline__ void chunk_zero(WarpChunk &st, int lane) {
+    double *w = &st.wx[0][0];
+    for (int i = lane; i < 24 * kChunk; i += 32) w[i] = 0.0;
+    __syncwarp();
+}
+
+// Coordinates of this lane's particle (c = x/h, i0 = ceil(c - w/2)).
 template <int W>
-__device__ __forceinline__ void stage_weights(WarpStage<W> &st, int lane, int p0, int cnt,
-                                              const double *__restrict__ px,
-                                              const double *__restrict__ py,
-                                              const double *__restrict__ pz,
-                                              const int64_t *__restrict__ pid,
-                                              const double *__restrict__ strengths, double q,
-                                              bool scale_x, double h, double beta) {
-    if (lane < 3 * kSub) {
-        const int j = lane / 3, d = lane - 3 * (lane / 3);
-        if (j < cnt) {
-            const double *src = d == 0 ? px : (d == 1 ? py : pz);
-            double c = axis_coord(src[p0 + j], h);
-            st.c[j][d] = c;
-            st.i0[j][d] = stencil_start(c, W);
+__device__ __forceinline__ void chunk_coords(WarpChunk &st, int lane, int cnt, double x, double y,
+                                             double z, double h, bool keep_x) {
+    if (lane < cnt) {
+        const double cx = axis_coord(x, h), cy = axis_coord(y, h), cz = axis_coord(z, h);
+        st.c[0][lane] = cx;
+        st.c[1][lane] = cy;
+        st.c[2][lane] = cz;
+        st.i0[0][lane] = stencil_start(cx, W);
+        st.i0[1][lane] = stencil_start(cy, W);
+        st.i0[2][lane] = stencil_start(cz, W);
+        if (keep_x) {
+            st.x[0][lane] = x;
+            st.x[1][lane] = y;
+            st.x[2][lane] = z;
         }
     }
     __syncwarp();
+}
+
+// The 3*W weights of each of the cnt particles, spread over the warp.
+template <int W>
+__device__ __forceinline__ void chunk_weights(WarpChunk &st, const double *tab, int lane, int cnt,
+                                              const double *sx, double beta) {
     constexpr double inv_half = 2.0 / W;
-#pragma unroll
-    for (int t0 = 0; t0 < kSub * 3 * W; t0 += 32) {
-        const int t = t0 + lane;
-        if (t < kSub * 3 * W) {
-            const int j = t / (3 * W);
-            const int r = t - j * (3 * W);
-            const int d = r / W;
-            const int a = r - d * W;
-            double v = 0.0;
-            if (j < cnt) {
-                v = es_weight(st.c[j][d], st.i0[j][d] + (double)a, inv_half, beta);
-                if (scale_x && d == 0) {
-                    double s = strengths ? strengths[pid[p0 + j]] : q;
-                    v = __dmul_rn(s, v);   // sa = s * wx[a] (_kernels.py:81)
-                }
-            }
-            st.wt[j][d][a] = v;
+    const int ntask = cnt * 3 * W;
+    for (int t = lane; t < ntask; t += 32) {
+        const int j = t / (3 * W);
+        const int r = t - j * (3 * W);
+        const int d = r / W;
+        const int a = r - d * W;
+        double v = es_weight_fast(st.c[d][j], st.i0[d][j] + (double)a, inv_half, beta, tab);
+        if (d == 0) {
+            if (sx) v = __dmul_rn(sx[j], v);   // sa = s * wx[a] (_kernels.py:81)
+            st.wx[a][j] = v;
+        } else if (d == 1) {
+            st.wy[a][j] = v;
+        } else {
+            st.wz[j][a] = v;
         }
     }
     __syncwarp();
 }
 
 // ----------------------------------------------------------------------------
-// fused spreading (w <= 8)
+// spreading (w <= 8) on the fp64 tensor cores
+//
+// Warp = one work item (z-segment of an (i0x, i0y) column of stencil cells).
+// For each stencil-x offset a, the 8 x 8 block G_a[b][z-slot] of the current
+// cell's footprint is one DMMA accumulator: G_a += A_a B over k-steps of 4
+// particles of that cell, with
+//   A_a[b][p] = (s_p wx_p[a]) wy_p[b]      (8 rows b  x 4 particles)
+//   B[p][s]   = wz_p[(s - k) mod 8]        (4 particles x 8 z-slots)
+// z-slot s holds plane z == s (mod 8): leaving cell k completes plane k
+// (slot k&7), which is flushed with REDG.ADD.F64 and reused for plane k+8.
 // ----------------------------------------------------------------------------
 
 template <int W>
+__device__ __forceinline__ void spread_flush_plane(double (&acc)[8][2], int k, int c4, int ix,
+                                                   int64_t yrow, int n, double *grid) {
+    const int s = k & 7;
+    if (c4 == (s >> 1)) {
+        const int j = s & 1;
+        const int z = k % n;
+#pragma unroll
+        for (int a = 0; a < W; ++a) {
+            const double v = j ? acc[a][1] : acc[a][0];
+            if (v != 0.0) atomicAdd(grid + ((int64_t)((ix + a) % n) * n + yrow) * n + z, v);
+        }
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            if (j) acc[a][1] = 0.0;
+            else acc[a][0] = 0.0;
+        }
+    }
+}
+
+template <int W>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
-spread_fast_kernel(const double *__restrict__ px, const double *__restrict__ py,
-                   const double *__restrict__ pz, const int64_t *__restrict__ pid,
-                   const double *__restrict__ strengths, double q,
-                   const int32_t *__restrict__ cell_start, double *__restrict__ grid, int n,
-                   int seg, int nseg, double h, double beta, unsigned int *work, int nitems) {
-    __shared__ WarpStage<W> stage[kWarpsPerBlock];
-    const int lane = threadIdx.x & 31;
-    WarpStage<W> &st = stage[threadIdx.x >> 5];
-    const int q0 = lane, q1 = lane + 32;
-    const bool v0 = q0 < W * W, v1 = q1 < W * W;
-    const int a0 = v0 ? q0 / W : 0, b0 = v0 ? q0 % W : 0;
-    const int a1 = v1 ? q1 / W : 0, b1 = v1 ? q1 % W : 0;
+spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
+                  const double *__restrict__ pz, const int64_t *__restrict__ pid,
+                  const double *__restrict__ strengths, double q,
+                  const int32_t *__restrict__ cell_start, double *__restrict__ grid, int n,
+                  int seg, int nseg, double h, double beta, unsigned int *work, int nitems) {
+    __shared__ WarpChunk stage[kWarpsPerBlock];
+    __shared__ double sstr[kWarpsPerBlock][kChunk];
+    __shared__ double tab[32];
+    if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    WarpChunk &st = stage[wib];
+    double *sx = sstr[wib];
+    chunk_zero(st, lane);
+    const int r = lane >> 2, c4 = lane & 3;
 
     for (;;) {
         int item = 0;
@@ -159,54 +218,82 @@ spread_fast_kernel(const double *__restrict__ px, const double *__restrict__ py,
         const int ix = col / n, iy = col - ix * n;
         const int k0 = sg * seg, k1 = min(k0 + seg, n);
         const int base = col * n;
-        if (cell_start[base + k0] == cell_start[base + k1]) continue;
+        const int pbeg = cell_start[base + k0], pend = cell_start[base + k1];
+        if (pbeg == pend) continue;
+        const int64_t yrow = (iy + r) % n;   // this lane's footprint row b = r
 
-        const int64_t row0 = ((int64_t)((ix + a0) % n) * n + (iy + b0) % n) * n;
-        const int64_t row1 = ((int64_t)((ix + a1) % n) * n + (iy + b1) % n) * n;
-        double acc0[W], acc1[W];
+        double acc[8][2];
 #pragma unroll
-        for (int s = 0; s < W; ++s) acc0[s] = acc1[s] = 0.0;
+        for (int a = 0; a < 8; ++a) acc[a][0] = acc[a][1] = 0.0;
+        int k = k0;
+        int cell_end = cell_start[base + k0 + 1];
 
-        for (int k = k0; k < k1; ++k) {
-            const int cs = cell_start[base + k], ce = cell_start[base + k + 1];
-            for (int p0 = cs; p0 < ce; p0 += kSub) {
-                const int cnt = min(kSub, ce - p0);
-                stage_weights<W>(st, lane, p0, cnt, px, py, pz, pid, strengths, q, true, h, beta);
-                for (int j = 0; j < cnt; ++j) {
-                    // sab = (s * wx[a]) * wy[b]; grid += sab * wz[c]  (_kernels.py:81-87)
-                    const double s0 = st.wt[j][0][a0] * st.wt[j][1][b0];
-                    const double s1 = st.wt[j][0][a1] * st.wt[j][1][b1];
-#pragma unroll
-                    for (int c = 0; c < W; ++c) {
-                        const double wz = st.wt[j][2][c];
-                        acc0[c] = fma(s0, wz, acc0[c]);
-                        acc1[c] = fma(s1, wz, acc1[c]);
-                    }
-                }
-                __syncwarp();
-            }
-            // plane k is complete: flush slot 0, rotate the window by one plane
-            const int z = k;  // k < n
-            if (v0 && acc0[0] != 0.0) atomicAdd(grid + row0 + z, acc0[0]);
-            if (v1 && acc1[0] != 0.0) atomicAdd(grid + row1 + z, acc1[0]);
-#pragma unroll
-            for (int s = 0; s + 1 < W; ++s) {
-                acc0[s] = acc0[s + 1];
-                acc1[s] = acc1[s + 1];
-            }
-            acc0[W - 1] = acc1[W - 1] = 0.0;
+        double nx = 0.0, ny = 0.0, nz = 0.0, ns = q;
+        if (pbeg + lane < pend) {
+            const int i = pbeg + lane;
+            nx = px[i];
+            ny = py[i];
+            nz = pz[i];
+            if (strengths) ns = strengths[pid[i]];
         }
+        for (int pos = pbeg; pos < pend; pos += kChunk) {
+            const int cnt = min(kChunk, pend - pos);
+            chunk_coords<W>(st, lane, cnt, nx, ny, nz, h, false);
+            sx[lane] = ns;
+            if (pos + kChunk + lane < pend) {   // prefetch the next chunk
+                const int i = pos + kChunk + lane;
+                nx = px[i];
+                ny = py[i];
+                nz = pz[i];
+                if (strengths) ns = strengths[pid[i]];
+            }
+            chunk_weights<W>(st, tab, lane, cnt, sx, beta);
+            int j = 0;
+            while (j < cnt) {
+                const int gp = pos + j;
+                if (gp >= cell_end) {
+                    spread_flush_plane<W>(acc, k, c4, ix, yrow, n, grid);
+                    ++k;
+                    cell_end = cell_start[base + k + 1];
+                    continue;
+                }
+                const int m = min(4, min(pos + cnt, cell_end) - gp);
+                const bool ok = c4 < m;
+                const int pj = ok ? j + c4 : j;
+                const double wyb = ok ? st.wy[r][pj] : 0.0;
+                const double bz = st.wz[pj][(r - k) & 7];
 #pragma unroll
-        for (int s = 0; s + 1 < W; ++s) {
-            const int z = (k1 + s) % n;
-            if (v0 && acc0[s] != 0.0) atomicAdd(grid + row0 + z, acc0[s]);
-            if (v1 && acc1[s] != 0.0) atomicAdd(grid + row1 + z, acc1[s]);
+                for (int a = 0; a < 8; ++a) dmma884(acc[a][0], acc[a][1], st.wx[a][pj] * wyb, bz);
+                j += m;
+            }
+            __syncwarp();
+        }
+        for (; k < k1; ++k) spread_flush_plane<W>(acc, k, c4, ix, yrow, n, grid);
+        // pending planes k1 .. k1+6
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int s = 2 * c4 + j;
+            const int z = (k1 + ((s - k1) & 7)) % n;
+#pragma unroll
+            for (int a = 0; a < W; ++a) {
+                const double v = acc[a][j];
+                if (v != 0.0) atomicAdd(grid + ((int64_t)((ix + a) % n) * n + yrow) * n + z, v);
+            }
         }
     }
 }
 
 // ----------------------------------------------------------------------------
-// fused gather (+ Boris push) (w <= 8)
+// gather (+ Boris push) (w <= 8) on the fp64 tensor cores
+//
+// The field window of the current cell (8 a x 8 b x 8 z-slots x 3 components)
+// lives in registers as DMMA A fragments: A_{a,h,d}[b][c'] = E_d(a, b, slot
+// c' + 4h).  For a sub-batch of up to 8 particles of the cell,
+// B_{a,h}[c'][p] = wx_p[a] wz_p[(c' + 4h - k) mod 8], so 16 DMMAs per component
+// accumulate D_d[b][p] = sum_{a,c} E_d(a,b,c) wx_p[a] wz_p[c]; the remaining
+// wy_p[b] contraction is 6 products and a 3-level butterfly over the b lanes.
+// Gathered fields go to shared memory; then every lane pushes one particle of
+// the chunk (coalesced loads/stores).
 // ----------------------------------------------------------------------------
 
 struct PushParams {
@@ -278,55 +365,36 @@ __device__ __forceinline__ void block_diag_store(double *dg, double *partials) {
     }
 }
 
-// Transposed warp reduction of part[kSub][3]: after it, every lane of group
-// g = (lane >> 2) & 7 holds the full 32-lane sum for particle g.
-__device__ __forceinline__ void reduce_scatter8(double (&part)[kSub][3], int lane, double *e) {
-    double r1[4][3], r2[2][3];
-    const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+__device__ __forceinline__ void load_plane(double (&g)[8][2][3], int hh, const double4 *field,
+                                           int ix, int64_t yrow, int n, int64_t z) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            double keep = h16 ? part[j + 4][d] : part[j][d];
-            double send = h16 ? part[j][d] : part[j + 4][d];
-            r1[j][d] = keep + __shfl_xor_sync(kFull, send, 16);
-        }
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            double keep = h8 ? r1[j + 2][d] : r1[j][d];
-            double send = h8 ? r1[j][d] : r1[j + 2][d];
-            r2[j][d] = keep + __shfl_xor_sync(kFull, send, 8);
-        }
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        double keep = h4 ? r2[1][d] : r2[0][d];
-        double send = h4 ? r2[0][d] : r2[1][d];
-        double v = keep + __shfl_xor_sync(kFull, send, 4);
-        v += __shfl_xor_sync(kFull, v, 2);
-        v += __shfl_xor_sync(kFull, v, 1);
-        e[d] = v;
+    for (int a = 0; a < 8; ++a) {
+        int xa = ix + a;
+        xa = xa >= n ? xa - n : xa;
+        const double4 f = field[((int64_t)xa * n + yrow) * n + z];
+        g[a][hh][0] = f.x;
+        g[a][hh][1] = f.y;
+        g[a][hh][2] = f.z;
     }
 }
 
 template <int W, bool PUSH>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
-interp_fast_kernel(pif_soa_t P, const int32_t *__restrict__ cell_start,
-                   const double4 *__restrict__ field, int seg, int nseg, double beta,
-                   PushParams pp, int32_t *__restrict__ key, int32_t *__restrict__ rank,
-                   int32_t *__restrict__ count, double *__restrict__ partials,
-                   double *__restrict__ E_out, unsigned int *work, int nitems) {
-    __shared__ WarpStage<W> stage[kWarpsPerBlock];
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
+interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ cell_start,
+                  const double4 *__restrict__ field, int seg, int nseg, double beta,
+                  PushParams pp, int32_t *__restrict__ key, int32_t *__restrict__ rank,
+                  int32_t *__restrict__ count, double *__restrict__ partials,
+                  double *__restrict__ E_out, unsigned int *work, int nitems) {
+    __shared__ WarpChunk stage[kWarpsPerBlock];
+    __shared__ double tab[32];
+    if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
+    __syncthreads();
     const int lane = threadIdx.x & 31;
-    WarpStage<W> &st = stage[threadIdx.x >> 5];
+    WarpChunk &st = stage[threadIdx.x >> 5];
+    chunk_zero(st, lane);
     const int n = pp.n;
     const double h = pp.h;
-    const int q0 = lane, q1 = lane + 32;
-    const bool v0 = q0 < W * W, v1 = q1 < W * W;
-    const int a0 = v0 ? q0 / W : 0, b0 = v0 ? q0 % W : 0;
-    const int a1 = v1 ? q1 / W : 0, b1 = v1 ? q1 % W : 0;
-    const int grp = (lane >> 2) & 7;
+    const int r = lane >> 2, c4 = lane & 3;
     double dg[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 
     for (;;) {
@@ -338,85 +406,116 @@ interp_fast_kernel(pif_soa_t P, const int32_t *__restrict__ cell_start,
         const int ix = col / n, iy = col - ix * n;
         const int k0 = sg * seg, k1 = min(k0 + seg, n);
         const int base = col * n;
-        if (cell_start[base + k0] == cell_start[base + k1]) continue;
+        const int pbeg = cell_start[base + k0], pend = cell_start[base + k1];
+        if (pbeg == pend) continue;
+        const int64_t yrow = (iy + r) % n;
 
-        const int64_t row0 = ((int64_t)((ix + a0) % n) * n + (iy + b0) % n) * n;
-        const int64_t row1 = ((int64_t)((ix + a1) % n) * n + (iy + b1) % n) * n;
-        // window of W planes: g0/g1[s] = field at plane k + s for the two pairs
-        double g0[W][3], g1[W][3];
-#pragma unroll
-        for (int s = 0; s < W; ++s) {
-            const int z = (k0 + s) % n;
-            double4 f0 = v0 ? field[row0 + z] : make_double4(0, 0, 0, 0);
-            double4 f1 = v1 ? field[row1 + z] : make_double4(0, 0, 0, 0);
-            g0[s][0] = f0.x; g0[s][1] = f0.y; g0[s][2] = f0.z;
-            g1[s][0] = f1.x; g1[s][1] = f1.y; g1[s][2] = f1.z;
+        // prefetch the first chunk (positions, velocities) before the window
+        double nx = 0.0, ny = 0.0, nz = 0.0, nvx = 0.0, nvy = 0.0, nvz = 0.0;
+        if (pbeg + lane < pend) {
+            const int i = pbeg + lane;
+            nx = P.x[i]; ny = P.y[i]; nz = P.z[i];
+            if (PUSH) { nvx = P.vx[i]; nvy = P.vy[i]; nvz = P.vz[i]; }
         }
-        for (int k = k0; k < k1; ++k) {
-            if (k > k0) {
+        // window: slot s = c4 + 4h holds plane z == s (mod 8) of [k0, k0+8)
+        double g[8][2][3];
 #pragma unroll
-                for (int s = 0; s + 1 < W; ++s)
+        for (int hh = 0; hh < 2; ++hh) {
+            const int s = c4 + 4 * hh;
+            load_plane(g, hh, field, ix, yrow, n, (k0 + ((s - k0) & 7)) % n);
+        }
+        int k = k0;
+        int cell_end = cell_start[base + k0 + 1];
+
+        for (int pos = pbeg; pos < pend; pos += kChunk) {
+            const int cnt = min(kChunk, pend - pos);
+            chunk_coords<W>(st, lane, cnt, nx, ny, nz, h, PUSH);
+            const double vx0 = nvx, vy0 = nvy, vz0 = nvz;
+            if (pos + kChunk + lane < pend) {   // prefetch the next chunk
+                const int i = pos + kChunk + lane;
+                nx = P.x[i]; ny = P.y[i]; nz = P.z[i];
+                if (PUSH) { nvx = P.vx[i]; nvy = P.vy[i]; nvz = P.vz[i]; }
+            }
+            chunk_weights<W>(st, tab, lane, cnt, nullptr, beta);
+            int j = 0;
+            while (j < cnt) {
+                const int gp = pos + j;
+                if (gp >= cell_end) {   // next cell: plane k leaves slot k&7, plane k+8 enters
+                    const int s = k & 7;
+                    if (c4 == (s & 3)) {
+                        const int64_t z = (k + 8) % n;
+                        if (s >> 2) load_plane(g, 1, field, ix, yrow, n, z);
+                        else load_plane(g, 0, field, ix, yrow, n, z);
+                    }
+                    ++k;
+                    cell_end = cell_start[base + k + 1];
+                    continue;
+                }
+                const int m = min(8, min(pos + cnt, cell_end) - gp);
+                const int pb = r < m ? j + r : j;          // B column p = r
+                const double bzs = r < m ? 1.0 : 0.0;
+                const double bz0 = bzs * st.wz[pb][(c4 - k) & 7];
+                const double bz1 = bzs * st.wz[pb][(c4 + 4 - k) & 7];
+                double D[2][3][2];
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) D[hh][d][0] = D[hh][d][1] = 0.0;
+#pragma unroll
+                for (int a = 0; a < 8; ++a) {
+                    const double wxa = st.wx[a][pb];
+                    const double b0 = wxa * bz0, b1 = wxa * bz1;
 #pragma unroll
                     for (int d = 0; d < 3; ++d) {
-                        g0[s][d] = g0[s + 1][d];
-                        g1[s][d] = g1[s + 1][d];
-                    }
-                const int z = (k + W - 1) % n;
-                double4 f0 = v0 ? field[row0 + z] : make_double4(0, 0, 0, 0);
-                double4 f1 = v1 ? field[row1 + z] : make_double4(0, 0, 0, 0);
-                g0[W - 1][0] = f0.x; g0[W - 1][1] = f0.y; g0[W - 1][2] = f0.z;
-                g1[W - 1][0] = f1.x; g1[W - 1][1] = f1.y; g1[W - 1][2] = f1.z;
-            }
-            const int cs = cell_start[base + k], ce = cell_start[base + k + 1];
-            for (int p0 = cs; p0 < ce; p0 += kSub) {
-                const int cnt = min(kSub, ce - p0);
-                stage_weights<W>(st, lane, p0, cnt, P.x, P.y, P.z, P.id, nullptr, 0.0, false, h,
-                                 beta);
-                double part[kSub][3];
-#pragma unroll
-                for (int j = 0; j < kSub; ++j) {
-                    if (j < cnt) {
-                        double h0[3] = {0.0, 0.0, 0.0}, h1[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-                        for (int c = 0; c < W; ++c) {
-                            const double wz = st.wt[j][2][c];
-#pragma unroll
-                            for (int d = 0; d < 3; ++d) {
-                                h0[d] = fma(g0[c][d], wz, h0[d]);
-                                h1[d] = fma(g1[c][d], wz, h1[d]);
-                            }
-                        }
-                        const double w0 = st.wt[j][0][a0] * st.wt[j][1][b0];
-                        const double w1 = v1 ? st.wt[j][0][a1] * st.wt[j][1][b1] : 0.0;
-#pragma unroll
-                        for (int d = 0; d < 3; ++d) part[j][d] = fma(w0, h0[d], w1 * h1[d]);
-                    } else {
-#pragma unroll
-                        for (int d = 0; d < 3; ++d) part[j][d] = 0.0;
+                        dmma884(D[0][d][0], D[0][d][1], g[a][0][d], b0);
+                        dmma884(D[1][d][0], D[1][d][1], g[a][1][d], b1);
                     }
                 }
-                double e[3];
-                reduce_scatter8(part, lane, e);
-                if ((lane & 3) == 0 && grp < cnt) {
-                    const int64_t i = p0 + grp;
-                    if (PUSH) {
-                        double x = P.x[i], y = P.y[i], z = P.z[i];
-                        double vx = P.vx[i], vy = P.vy[i], vz = P.vz[i];
-                        boris_one(pp, e[0], e[1], e[2], x, y, z, vx, vy, vz, dg);
-                        P.x[i] = x; P.y[i] = y; P.z[i] = z;
-                        P.vx[i] = vx; P.vy[i] = vy; P.vz[i] = vz;
-                        const int kk = cell_key(x, y, z, h, pp.w, n);
-                        key[i] = kk;
-                        rank[i] = atomicAdd(&count[kk], 1);
-                    } else {
-                        const int64_t o = 3 * P.id[i];
-                        E_out[o] = e[0];
-                        E_out[o + 1] = e[1];
-                        E_out[o + 2] = e[2];
-                    }
+                // E_d[p] = sum_b wy_p[b] D_d[b][p], p = 2*c4 + i, b = r
+                const int q0 = min(j + 2 * c4, kChunk - 1), q1 = min(j + 2 * c4 + 1, kChunk - 1);
+                const double wy0 = st.wy[r][q0], wy1 = st.wy[r][q1];
+                double e[3][2];
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    e[d][0] = wy0 * (D[0][d][0] + D[1][d][0]);
+                    e[d][1] = wy1 * (D[0][d][1] + D[1][d][1]);
                 }
-                __syncwarp();
+#pragma unroll
+                for (int o = 4; o < 32; o <<= 1)
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) {
+                        e[d][0] += __shfl_xor_sync(kFull, e[d][0], o);
+                        e[d][1] += __shfl_xor_sync(kFull, e[d][1], o);
+                    }
+                const int pl = 2 * c4 + r;   // particle written by this lane (r < 2)
+                if (r < 2 && pl < m) {
+                    st.E[0][j + pl] = r ? e[0][1] : e[0][0];
+                    st.E[1][j + pl] = r ? e[1][1] : e[1][0];
+                    st.E[2][j + pl] = r ? e[2][1] : e[2][0];
+                }
+                j += m;
             }
+            __syncwarp();
+            if (lane < cnt) {
+                const int64_t i = pos + lane;
+                const double E0 = st.E[0][lane], E1 = st.E[1][lane], E2 = st.E[2][lane];
+                if (PUSH) {
+                    double x = st.x[0][lane], y = st.x[1][lane], z = st.x[2][lane];
+                    double vx = vx0, vy = vy0, vz = vz0;
+                    boris_one(pp, E0, E1, E2, x, y, z, vx, vy, vz, dg);
+                    P.x[i] = x; P.y[i] = y; P.z[i] = z;
+                    P.vx[i] = vx; P.vy[i] = vy; P.vz[i] = vz;
+                    const int kk = cell_key(x, y, z, h, pp.w, n);
+                    key[i] = kk;
+                    rank[i] = atomicAdd(&count[kk], 1);
+                } else {
+                    const int64_t o = 3 * P.id[i];
+                    E_out[o] = E0;
+                    E_out[o + 1] = E1;
+                    E_out[o + 2] = E2;
+                }
+            }
+            __syncwarp();
         }
     }
     if (PUSH) block_diag_store(dg, partials);
@@ -680,7 +779,7 @@ int launch_spread(Plan &p, const pif_soa_t &P, const double *strengths, double q
         const int threads = kWarpsPerBlock * 32;
 #define PIF_SPREAD_CASE(W)                                                                   \
     case W: {                                                                                \
-        auto k = spread_fast_kernel<W>;                                                      \
+        auto k = spread_mma_kernel<W>;                                                      \
         int blocks = persistent_blocks(k, threads, 0, p.sm_count);                           \
         k<<<blocks, threads, 0, s>>>(P.x, P.y, P.z, P.id, strengths, q, p.cell_start, p.grid, \
                                      p.n, p.seg, nseg, p.h, p.beta, p.work, nitems);         \
@@ -726,14 +825,14 @@ int launch_interp(Plan &p, pif_soa_t &P, bool push, double half, double dt, cons
 #define PIF_INTERP_CASE(W)                                                                    \
     case W: {                                                                                 \
         if (push) {                                                                           \
-            auto k = interp_fast_kernel<W, true>;                                             \
+            auto k = interp_mma_kernel<W, true>;                                             \
             blocks = persistent_blocks(k, threads, 0, p.sm_count);                            \
             if (blocks > p.partial_blocks) blocks = p.partial_blocks;                         \
             k<<<blocks, threads, 0, s>>>(P, p.cell_start, field, p.seg, nseg, p.beta, pp, key, \
                                          rank, p.cell_count, p.partials, E_out, p.work,        \
                                          nitems);                                             \
         } else {                                                                              \
-            auto k = interp_fast_kernel<W, false>;                                            \
+            auto k = interp_mma_kernel<W, false>;                                            \
             blocks = persistent_blocks(k, threads, 0, p.sm_count);                            \
             k<<<blocks, threads, 0, s>>>(P, p.cell_start, field, p.seg, nseg, p.beta, pp, key, \
                                          rank, p.cell_count, p.partials, E_out, p.work,        \

@@ -112,7 +112,7 @@ class PifEngine:
         _native.call("pif_bin_scatter", self.handle, ctypes.byref(src), ctypes.byref(dst),
                      self.parts.key.data_ptr(), self.parts.rank.data_ptr(), 1, self._stream())
         self.parts.swap()
-        self.launches += 2
+        self.launches += 3      # CUB scan (2 kernels) + scatter
 
     # -- stages -----------------------------------------------------------------
     def particle_diag(self):
@@ -121,13 +121,22 @@ class PifEngine:
                      self.diag.data_ptr(), self._stream())
         self.launches += 2
 
-    def deposit(self):
-        """Scatter: binned spreading + D2Z + truncate/deconvolve -> raw modes."""
+    def spread(self):
+        """Binned register-tiled spreading into the plan's fine grid."""
         cur = self._soa()
-        s = self._stream()
-        _native.call("pif_spread_sorted", self.handle, ctypes.byref(cur), None, self.q, s)
-        _native.call("pif_grid_to_modes", self.handle, self.raw.data_ptr(), s)
-        self.launches += 3
+        _native.call("pif_spread_sorted", self.handle, ctypes.byref(cur), None, self.q,
+                     self._stream())
+        self.launches += 1
+
+    def modes(self):
+        """cuFFT D2Z + truncate/deconvolve -> raw modes (head of the allreduce buffer)."""
+        _native.call("pif_grid_to_modes", self.handle, self.raw.data_ptr(), self._stream())
+        self.launches += 1
+
+    def deposit(self):
+        """Scatter stage: spread + modes."""
+        self.spread()
+        self.modes()
 
     def allreduce(self):
         if self.comm is not None:
@@ -137,17 +146,24 @@ class PifEngine:
         """finish_deposit + Poisson + energy + guard + padded spectra + Z2D."""
         _native.call("pif_solve_fields", self.handle, self.raw.data_ptr(), self.shape,
                      self.rho.data_ptr(), self.scalars.data_ptr(), self._stream())
-        self.launches += 6
+        self.launches += 5      # poisson, energy, guard (2), pad; cuFFT Z2D not counted
 
-    def gather_push(self):
-        """Fused gather + Boris push, then bin the new positions."""
+    def interp_push(self):
+        """Fused gather + Boris push + next cell keys + diagnostic sums."""
         cur = self._soa()
         _native.call("pif_interp_push", self.handle, ctypes.byref(cur), self.half, self.dt,
                      self._tq, self._sq, self.has_b, self.e_kind, self.parts.key.data_ptr(),
                      self.parts.rank.data_ptr(), self.diag.data_ptr(), self._stream())
         self.launches += 2
+
+    def rebin(self):
+        """Scan the cell counts emitted by interp_push and scatter into cell order."""
         if self.count:
             self._scatter()
+
+    def gather_push(self):
+        self.interp_push()
+        self.rebin()
 
     def record(self, slot: int):
         r = self.rec[slot]
