@@ -92,67 +92,52 @@ __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double
 }
 
 // Per-warp staging of one chunk of up to kChunk consecutive (cell-sorted)
-// particles of a work item; chunks run across cell boundaries.  Weights are
-// padded to 8 with zeros (rows a >= w are never written), laid out for the
-// fragment loads.
+// particles of a work item; chunks run across cell boundaries.  Lane j owns
+// particle j of the chunk: it loads it, computes its 3 x w window weights and
+// (gather) pushes it.  Weights are padded to 8 with zeros (entries a >= w are
+// never written) and laid out so the DMMA fragment loads are conflict-free or
+// 2-way (row strides 33 and 9 doubles).
 constexpr int kChunk = 32;
 
 struct WarpChunk {
-    double wx[8][kChunk];   // [a][p]  x weights (spreading: times the strength)
-    double wy[8][kChunk];   // [b][p]
-    double wz[kChunk][8];   // [p][c]
-    double c[3][kChunk];    // coordinates in grid units
-    double i0[3][kChunk];   // stencil starts
-    double x[3][kChunk];    // positions (gather+push)
-    double E[3][kChunk];    // gathered field (gather+push)
+    double wx[8][kChunk + 1];   // [a][p]  x weights (spreading: times the strength)
+    double wy[kChunk][9];       // [p][b]
+    double wz[kChunk][9];       // [p][c]
+    double E[3][kChunk];        // gathered field (gather+push)
 };
 
 __device__ __forceinline__ void chunk_zero(WarpChunk &st, int lane) {
     double *w = &st.wx[0][0];
-    for (int i = lane; i < 24 * kChunk; i += 32) w[i] = 0.0;
+    const int nw = 8 * (kChunk + 1) + 2 * kChunk * 9;
+    for (int i = lane; i < nw; i += 32) w[i] = 0.0;
     __syncwarp();
 }
 
-// Coordinates of this lane's particle (c = x/h, i0 = ceil(c - w/2)).
-template <int W>
-__device__ __forceinline__ void chunk_coords(WarpChunk &st, int lane, int cnt, double x, double y,
-                                             double z, double h, bool keep_x) {
-    if (lane < cnt) {
-        const double cx = axis_coord(x, h), cy = axis_coord(y, h), cz = axis_coord(z, h);
-        st.c[0][lane] = cx;
-        st.c[1][lane] = cy;
-        st.c[2][lane] = cz;
-        st.i0[0][lane] = stencil_start(cx, W);
-        st.i0[1][lane] = stencil_start(cy, W);
-        st.i0[2][lane] = stencil_start(cz, W);
-        if (keep_x) {
-            st.x[0][lane] = x;
-            st.x[1][lane] = y;
-            st.x[2][lane] = z;
-        }
-    }
-    __syncwarp();
-}
-
-// The 3*W weights of each of the cnt particles, spread over the warp.
+// Window weights of this lane's particle (lane < cnt): c = x/h, i0 = ceil(c - w/2),
+// w weights per axis (_kernels.py:11-28), x row scaled by the strength s.
 template <int W>
 __device__ __forceinline__ void chunk_weights(WarpChunk &st, const double *tab, int lane, int cnt,
-                                              const double *sx, double beta) {
+                                              double x, double y, double z, double s, bool scale,
+                                              double h, double beta) {
     constexpr double inv_half = 2.0 / W;
-    const int ntask = cnt * 3 * W;
-    for (int t = lane; t < ntask; t += 32) {
-        const int j = t / (3 * W);
-        const int r = t - j * (3 * W);
-        const int d = r / W;
-        const int a = r - d * W;
-        double v = es_weight_fast(st.c[d][j], st.i0[d][j] + (double)a, inv_half, beta, tab);
-        if (d == 0) {
-            if (sx) v = __dmul_rn(sx[j], v);   // sa = s * wx[a] (_kernels.py:81)
-            st.wx[a][j] = v;
-        } else if (d == 1) {
-            st.wy[a][j] = v;
-        } else {
-            st.wz[j][a] = v;
+    if (lane < cnt) {
+        const double xyz[3] = {x, y, z};
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const double c = axis_coord(xyz[d], h);
+            const double i0 = stencil_start(c, W);
+#pragma unroll
+            for (int a = 0; a < W; ++a) {
+                double v = es_weight_fast(c, i0 + (double)a, inv_half, beta, tab);
+                if (d == 0) {
+                    if (scale) v = __dmul_rn(s, v);   // sa = s * wx[a] (_kernels.py:81)
+                    st.wx[a][lane] = v;
+                } else if (d == 1) {
+                    st.wy[lane][a] = v;
+                } else {
+                    st.wz[lane][a] = v;
+                }
+            }
         }
     }
     __syncwarp();
@@ -199,13 +184,11 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
                   const int32_t *__restrict__ cell_start, double *__restrict__ grid, int n,
                   int seg, int nseg, double h, double beta, unsigned int *work, int nitems) {
     __shared__ WarpChunk stage[kWarpsPerBlock];
-    __shared__ double sstr[kWarpsPerBlock][kChunk];
     __shared__ double tab[32];
     if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
     __syncthreads();
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    WarpChunk &st = stage[wib];
-    double *sx = sstr[wib];
+    const int lane = threadIdx.x & 31;
+    WarpChunk &st = stage[threadIdx.x >> 5];
     chunk_zero(st, lane);
     const int r = lane >> 2, c4 = lane & 3;
 
@@ -238,8 +221,7 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
         }
         for (int pos = pbeg; pos < pend; pos += kChunk) {
             const int cnt = min(kChunk, pend - pos);
-            chunk_coords<W>(st, lane, cnt, nx, ny, nz, h, false);
-            sx[lane] = ns;
+            const double cx = nx, cy = ny, cz = nz, cs = ns;
             if (pos + kChunk + lane < pend) {   // prefetch the next chunk
                 const int i = pos + kChunk + lane;
                 nx = px[i];
@@ -247,7 +229,7 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
                 nz = pz[i];
                 if (strengths) ns = strengths[pid[i]];
             }
-            chunk_weights<W>(st, tab, lane, cnt, sx, beta);
+            chunk_weights<W>(st, tab, lane, cnt, cx, cy, cz, cs, true, h, beta);
             int j = 0;
             while (j < cnt) {
                 const int gp = pos + j;
@@ -260,7 +242,7 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
                 const int m = min(4, min(pos + cnt, cell_end) - gp);
                 const bool ok = c4 < m;
                 const int pj = ok ? j + c4 : j;
-                const double wyb = ok ? st.wy[r][pj] : 0.0;
+                const double wyb = ok ? st.wy[pj][r] : 0.0;
                 const double bz = st.wz[pj][(r - k) & 7];
 #pragma unroll
                 for (int a = 0; a < 8; ++a) dmma884(acc[a][0], acc[a][1], st.wx[a][pj] * wyb, bz);
@@ -429,14 +411,13 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ cell_start,
 
         for (int pos = pbeg; pos < pend; pos += kChunk) {
             const int cnt = min(kChunk, pend - pos);
-            chunk_coords<W>(st, lane, cnt, nx, ny, nz, h, PUSH);
-            const double vx0 = nvx, vy0 = nvy, vz0 = nvz;
+            const double x0 = nx, y0 = ny, z0 = nz, vx0 = nvx, vy0 = nvy, vz0 = nvz;
             if (pos + kChunk + lane < pend) {   // prefetch the next chunk
                 const int i = pos + kChunk + lane;
                 nx = P.x[i]; ny = P.y[i]; nz = P.z[i];
                 if (PUSH) { nvx = P.vx[i]; nvy = P.vy[i]; nvz = P.vz[i]; }
             }
-            chunk_weights<W>(st, tab, lane, cnt, nullptr, beta);
+            chunk_weights<W>(st, tab, lane, cnt, x0, y0, z0, 1.0, false, h, beta);
             int j = 0;
             while (j < cnt) {
                 const int gp = pos + j;
@@ -473,7 +454,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ cell_start,
                 }
                 // E_d[p] = sum_b wy_p[b] D_d[b][p], p = 2*c4 + i, b = r
                 const int q0 = min(j + 2 * c4, kChunk - 1), q1 = min(j + 2 * c4 + 1, kChunk - 1);
-                const double wy0 = st.wy[r][q0], wy1 = st.wy[r][q1];
+                const double wy0 = st.wy[q0][r], wy1 = st.wy[q1][r];
                 double e[3][2];
 #pragma unroll
                 for (int d = 0; d < 3; ++d) {
@@ -500,7 +481,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ cell_start,
                 const int64_t i = pos + lane;
                 const double E0 = st.E[0][lane], E1 = st.E[1][lane], E2 = st.E[2][lane];
                 if (PUSH) {
-                    double x = st.x[0][lane], y = st.x[1][lane], z = st.x[2][lane];
+                    double x = x0, y = y0, z = z0;
                     double vx = vx0, vy = vy0, vz = vz0;
                     boris_one(pp, E0, E1, E2, x, y, z, vx, vy, vz, dg);
                     P.x[i] = x; P.y[i] = y; P.z[i] = z;
