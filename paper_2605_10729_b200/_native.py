@@ -12,7 +12,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpifb200.so")
+LIB_PATH = os.environ.get("PIF_B200_LIB", os.path.join(_HERE, "libpifb200.so"))
 
 PIF_OK, PIF_ERR_VALUE, PIF_ERR_CUDA, PIF_ERR_STATE = 0, 1, 2, 3
 SHAPE = {"delta": 0, "cic": 1}

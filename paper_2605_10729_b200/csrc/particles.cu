@@ -86,7 +86,7 @@ __global__ void bin_scatter_kernel(pif_soa_t src, pif_soa_t dst, const int32_t *
 // A[row = lane>>2][col = lane&3], B[row = lane&3][col = lane>>2],
 // D[row = lane>>2][col = 2*(lane&3) + {0,1}] (checked by tools/dmma_probe.cu).
 __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                  : "+d"(d0), "+d"(d1)
                  : "d"(a), "d"(b));
 }
@@ -360,8 +360,55 @@ __device__ __forceinline__ void load_plane(double (&g)[8][2][3], int hh, const d
     }
 }
 
+// One sub-batch of up to m particles (<= 8) of cell k starting at chunk slot j.
+// DMMA with the particle weights as the A operand and the register window as
+// the B operand (the A and B fragment layouts are transposes of each other, so
+// lane (r, c4) holding E(a, b=r, slot c4+4h) is a valid B fragment):
+//   A_{a,h}[p][c'] = wx_p[a] wz_p[(c' + 4h - k) mod 8]    (p = r)
+//   D_d[p][b]     += A_{a,h} x B_{a,h,d}[c'][b]           (16 DMMAs per component)
+// then E_d(p) = sum_b wy_p[b] D_d[p][b]: one product pair per lane and a
+// 2-level butterfly over the 4 lanes sharing p.
+__device__ __forceinline__ void gather_sub(WarpChunk &st, const double (&g)[8][2][3], int j, int m,
+                                           int k, int r, int c4) {
+    const int pb = r < m ? j + r : j;
+    const double sc = r < m ? 1.0 : 0.0;
+    const double bz0 = sc * st.wz[pb][(c4 - k) & 7];
+    const double bz1 = sc * st.wz[pb][(c4 + 4 - k) & 7];
+    double D[3][2];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) D[d][0] = D[d][1] = 0.0;
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+        const double wxa = st.wx[a][pb];
+        const double a0 = wxa * bz0, a1 = wxa * bz1;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            dmma884(D[d][0], D[d][1], a0, g[a][0][d]);
+            dmma884(D[d][0], D[d][1], a1, g[a][1][d]);
+        }
+    }
+    const double wy0 = st.wy[pb][2 * c4], wy1 = st.wy[pb][2 * c4 + 1];
+    double e[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) e[d] = fma(wy1, D[d][1], wy0 * D[d][0]);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        e[d] += __shfl_xor_sync(kFull, e[d], 1);
+        e[d] += __shfl_xor_sync(kFull, e[d], 2);
+    }
+    if (c4 == 0 && r < m) {
+        st.E[0][j + r] = e[0];
+        st.E[1][j + r] = e[1];
+        st.E[2][j + r] = e[2];
+    }
+}
+
+#ifndef PIF_INTERP_MINB
+#define PIF_INTERP_MINB 2
+#endif
+
 template <int W, bool PUSH>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, PIF_INTERP_MINB)
 interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ cell_start,
                   const double4 *__restrict__ field, int seg, int nseg, double beta,
                   PushParams pp, int32_t *__restrict__ key, int32_t *__restrict__ rank,
@@ -433,47 +480,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ cell_start,
                     continue;
                 }
                 const int m = min(8, min(pos + cnt, cell_end) - gp);
-                const int pb = r < m ? j + r : j;          // B column p = r
-                const double bzs = r < m ? 1.0 : 0.0;
-                const double bz0 = bzs * st.wz[pb][(c4 - k) & 7];
-                const double bz1 = bzs * st.wz[pb][(c4 + 4 - k) & 7];
-                double D[2][3][2];
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh)
-#pragma unroll
-                    for (int d = 0; d < 3; ++d) D[hh][d][0] = D[hh][d][1] = 0.0;
-#pragma unroll
-                for (int a = 0; a < 8; ++a) {
-                    const double wxa = st.wx[a][pb];
-                    const double b0 = wxa * bz0, b1 = wxa * bz1;
-#pragma unroll
-                    for (int d = 0; d < 3; ++d) {
-                        dmma884(D[0][d][0], D[0][d][1], g[a][0][d], b0);
-                        dmma884(D[1][d][0], D[1][d][1], g[a][1][d], b1);
-                    }
-                }
-                // E_d[p] = sum_b wy_p[b] D_d[b][p], p = 2*c4 + i, b = r
-                const int q0 = min(j + 2 * c4, kChunk - 1), q1 = min(j + 2 * c4 + 1, kChunk - 1);
-                const double wy0 = st.wy[q0][r], wy1 = st.wy[q1][r];
-                double e[3][2];
-#pragma unroll
-                for (int d = 0; d < 3; ++d) {
-                    e[d][0] = wy0 * (D[0][d][0] + D[1][d][0]);
-                    e[d][1] = wy1 * (D[0][d][1] + D[1][d][1]);
-                }
-#pragma unroll
-                for (int o = 4; o < 32; o <<= 1)
-#pragma unroll
-                    for (int d = 0; d < 3; ++d) {
-                        e[d][0] += __shfl_xor_sync(kFull, e[d][0], o);
-                        e[d][1] += __shfl_xor_sync(kFull, e[d][1], o);
-                    }
-                const int pl = 2 * c4 + r;   // particle written by this lane (r < 2)
-                if (r < 2 && pl < m) {
-                    st.E[0][j + pl] = r ? e[0][1] : e[0][0];
-                    st.E[1][j + pl] = r ? e[1][1] : e[1][0];
-                    st.E[2][j + pl] = r ? e[2][1] : e[2][0];
-                }
+                gather_sub(st, g, j, m, k, r, c4);
                 j += m;
             }
             __syncwarp();
