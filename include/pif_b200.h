@@ -55,7 +55,9 @@ int pif_abi_version(void);
  * All scalars and (N,) tables are computed on the host by the caller exactly
  * as the reference computes them (numpy), so the device sees identical
  * constants; the plan owns the cuFFT plans, the fine
- * grid, spectra, the interleaved field grid and the cell tables on `device`. */
+ * grid, spectra, the interleaved field grid and the cell tables on `device`.
+ * A plan carries the state of one particle set between calls (cell table,
+ * field grid): use one plan per particle set / stream, not concurrently. */
 typedef struct {
     int N;                   /* modes per dimension (even, >= 4)               */
     double L;                /* periodic box length                            */

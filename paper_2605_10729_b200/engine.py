@@ -47,7 +47,12 @@ class PifEngine:
             raise ValueError(f"dt must be positive, got {dt}")
         self.plan = plan
         self.device = torch.device(device)
-        self.dp = plan.native(self.device)
+        # a native plan holds per-run state (cell tables, field grid, FFT work
+        # areas), so every engine owns one; the per-device plan cached on the
+        # NufftPlan is reserved for the sequential operator API
+        from .nufft import DevicePlan
+        idx = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        self.dp = DevicePlan(plan, idx)
         self.handle = self.dp.handle
         self.count = int(count)
         self.parts = DeviceParticles(self.count, self.device)

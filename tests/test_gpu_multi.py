@@ -1,0 +1,59 @@
+"""Particle decomposition across processes over NCCL (one rank per GPU), the
+torchrun layout bench.py uses.  Needs >= 2 GPUs; skipped otherwise."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_10729_b200 as pb
+    from paper_2605_10729_b200 import comm
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    log = comm.CallLog()
+    ctx = comm.context_from_env(call_log=log, backend="nccl")
+    spec = pb.landau_spec(N=16, ppm=16, dt=0.05, steps=20, seed=0)
+    res = pb.run_particle_decomposition(pb.RunSetup(spec=spec, eps=1e-7), ctx)
+    tr = None
+    if rank == 0:
+        tr = [[r.field_energy, r.kinetic_energy, r.total_energy]
+              for r in [res["initial"]] + res["records"]]
+    q.put((rank, tr, sorted(log.primitives()), len(log.records)))
+    dist.barrier()
+    dist.destroy_process_group()
+    del torch
+
+
+def test_nccl_pd_two_processes_matches_reference(cuda):
+    torch = cuda
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted((q.get(timeout=300) for _ in range(2)), key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+    ref = golden("config1.npz")["landau_pd2_trace"][:, 2:5]
+    got = np.array(out[0][1])
+    assert np.max(np.abs(got - ref) / np.abs(ref)) <= 1e-10
+    for rank, _, prims, n in out:
+        assert prims == ["allreduce"]
+        assert n == 21          # one collective per step (+ the priming solve)

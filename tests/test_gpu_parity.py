@@ -1,0 +1,451 @@
+"""Parity of the CUDA path (libpifb200 through the reference-style API) with the
+reference's golden vectors and the CPU oracle, plus the reference's own known
+answers and size-independent properties at benchmark sizes.
+
+Tolerances: the north-star contract is rho_hat and E-at-particles rel-L2
+<= 1e-8 (CONTRACT) and energy traces <= 1e-6 relative (TRACE); the assertions
+also hold the implementation to the ~1e-12 it actually reaches (TIGHT) so a
+regression shows long before the contract would fail.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden, oracle, rel_l2, rel_max
+
+import paper_2605_10729_b200 as pb
+from paper_2605_10729_b200 import nufft
+
+pytestmark = pytest.mark.gpu
+
+CONTRACT = 1e-8
+TRACE = 1e-6
+TIGHT = 1e-12
+
+CASES = golden("nufft_cases.npz")
+NCASE = len({k.split("_")[0] for k in CASES.files})
+CFG = golden("config1.npz")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _native_loaded(cuda):
+    from paper_2605_10729_b200 import _native
+    _native.load()
+
+
+def _plan(ci):
+    N, L, eps = CASES[f"c{ci}_meta"]
+    return pb.make_plan(int(N), float(L), float(eps))
+
+
+# ---------------------------------------------------------------------------
+# NUFFT operator API vs the reference's own outputs
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("ci", range(NCASE))
+def test_type1_real_matches_reference(ci):
+    got = pb.type1(_plan(ci), CASES[f"c{ci}_pts"], CASES[f"c{ci}_cr"]).coeffs
+    assert isinstance(got, np.ndarray)      # numpy in -> numpy out (reference API)
+    ref = CASES[f"c{ci}_t1_real"]
+    assert rel_l2(got, ref) <= CONTRACT
+    assert rel_max(got, ref) <= TIGHT
+
+
+@pytest.mark.parametrize("ci", range(NCASE))
+def test_type1_complex_matches_reference(ci):
+    got = pb.type1(_plan(ci), CASES[f"c{ci}_pts"], CASES[f"c{ci}_cc"]).coeffs
+    assert rel_max(got, CASES[f"c{ci}_t1_cplx"]) <= TIGHT
+
+
+@pytest.mark.parametrize("ci", range(NCASE))
+def test_type2_matches_reference(ci):
+    got = pb.type2(_plan(ci), CASES[f"c{ci}_f"], CASES[f"c{ci}_pts"])
+    assert rel_max(got, CASES[f"c{ci}_t2"]) <= TIGHT
+
+
+@pytest.mark.parametrize("ci", range(NCASE))
+def test_gather3_matches_reference(ci):
+    comps = [CASES[f"c{ci}_herm{d}"] for d in range(3)]
+    got = nufft.gather3_real(_plan(ci), comps, CASES[f"c{ci}_pts"])
+    assert rel_l2(got, CASES[f"c{ci}_g3"]) <= CONTRACT
+    assert rel_max(got, CASES[f"c{ci}_g3"]) <= TIGHT
+
+
+@pytest.mark.parametrize("ci", [i for i in range(NCASE) if f"c{i}_d1" in CASES.files])
+def test_direct_sums_match_reference(ci):
+    plan = _plan(ci)
+    assert rel_max(pb.direct_transform(plan, "type1", CASES[f"c{ci}_pts"],
+                                       CASES[f"c{ci}_cc"]).coeffs, CASES[f"c{ci}_d1"]) <= 1e-12
+    assert rel_max(nufft.direct_type2(plan, CASES[f"c{ci}_f"], CASES[f"c{ci}_pts"]),
+                   CASES[f"c{ci}_d2"]) <= 1e-12
+
+
+def test_device_tensors_in_device_tensors_out(cuda):
+    torch = cuda
+    plan = _plan(2)
+    pts = torch.as_tensor(CASES["c2_pts"], device="cuda")
+    c = torch.as_tensor(CASES["c2_cr"], device="cuda")
+    F = pb.type1(plan, pts, c)
+    assert F.coeffs.is_cuda
+    assert rel_max(F.coeffs.cpu().numpy(), CASES["c2_t1_real"]) <= TIGHT
+
+
+# ---------------------------------------------------------------------------
+# the reference's known answers (test_nufft.py, test_pif.py, test_spectral.py)
+# ---------------------------------------------------------------------------
+
+def test_type1_single_point_at_origin():
+    plan = pb.make_plan(8, 2 * np.pi, 1e-7)
+    F = pb.type1(plan, np.zeros((1, 3)), np.ones(1))
+    assert np.max(np.abs(F.coeffs - 1.0)) <= 10 * plan.eps
+
+
+def test_type1_empty_input():
+    plan = pb.make_plan(8, 2 * np.pi, 1e-7)
+    assert np.all(pb.type1(plan, np.zeros((0, 3)), np.zeros(0)).coeffs == 0)
+
+
+def test_type1_rejects_nonfinite():
+    plan = pb.make_plan(8, 2 * np.pi, 1e-7)
+    with pytest.raises(ValueError):
+        pb.type1(plan, np.array([[np.nan, 0, 0]]), np.ones(1))
+    with pytest.raises(ValueError):
+        pb.type1(plan, np.zeros((1, 3)), np.array([np.inf]))
+    with pytest.raises(ValueError):
+        pb.type1(plan, np.zeros((2, 3)), np.ones(3))
+
+
+def test_type2_constant_and_zero_field():
+    plan = pb.make_plan(8, 2 * np.pi, 1e-7)
+    N = plan.N
+    f = np.zeros((N,) * 3, complex)
+    f[N // 2, N // 2, N // 2] = 2.5 - 0.5j
+    pts = np.random.default_rng(13).random((20, 3)) * plan.L
+    assert np.max(np.abs(pb.type2(plan, f, pts) - (2.5 - 0.5j))) <= 10 * plan.eps * 2.6
+    assert np.all(pb.type2(plan, np.zeros((N,) * 3, complex), pts) == 0)
+
+
+@pytest.mark.parametrize("eps", [1e-3, 1e-6, 1e-7, 1e-12])
+def test_accuracy_vs_direct_sums(eps):
+    # acceptance criterion 1 (test_acceptance.py:67-83): <= 10 eps vs direct sums
+    rng = np.random.default_rng(101)
+    for N in (8, 16):
+        plan = pb.make_plan(N, 2 * np.pi, eps)
+        pts = rng.random((1000, 3)) * plan.L
+        c = rng.standard_normal(1000) + 1j * rng.standard_normal(1000)
+        F = pb.type1(plan, pts, c).coeffs
+        Fd = pb.direct_transform(plan, "type1", pts, c).coeffs
+        assert rel_max(F, Fd) <= 10 * eps
+        cr = rng.standard_normal(1000)
+        Fr = pb.type1(plan, pts, cr).coeffs
+        assert rel_max(Fr, pb.direct_transform(plan, "type1", pts, cr).coeffs) <= 10 * eps
+        f = rng.standard_normal((N,) * 3) + 1j * rng.standard_normal((N,) * 3)
+        assert rel_max(pb.type2(plan, f, pts), nufft.direct_type2(plan, f, pts)) <= 10 * eps
+
+
+def test_conjugate_symmetry_real_strengths():
+    from paper_2605_10729_b200.spectral import hermitian_mismatch
+    plan = pb.make_plan(8, 2 * np.pi, 1e-7)
+    rng = np.random.default_rng(12)
+    F = pb.type1(plan, rng.random((40, 3)) * plan.L, rng.standard_normal(40)).coeffs
+    assert hermitian_mismatch(F) <= 1e-13 * np.max(np.abs(F))
+
+
+def _ens(x, v=None, q=-1.0, m=1.0):
+    x = np.atleast_2d(np.asarray(x, float))
+    v = np.zeros_like(x) if v is None else np.atleast_2d(np.asarray(v, float))
+    n = x.shape[0]
+    return pb.ParticleEnsemble(x=x, v=v, ids=np.arange(n), q_per_particle=q, m_per_particle=m,
+                               total_charge=q * n, total_mass=m * n, global_count=n)
+
+
+def test_deposit_single_particle_and_cancellation():
+    plan = pb.make_plan(8, 2 * np.pi, 1e-7)
+    rho = pb.deposit_charge(_ens([[0.0, 0.0, 0.0]], q=-2.0), plan).coeffs
+    mid = plan.N // 2
+    assert rho[mid, mid, mid] == 0.0
+    mask = np.ones(rho.shape, bool)
+    mask[mid, mid, mid] = False
+    expect = -2.0 / plan.L ** 3
+    assert np.max(np.abs(rho[mask] - expect)) <= 10 * plan.eps * abs(expect)
+    x = [[1.0, 2.0, 3.0]]
+    plus = pb.deposit_charge(_ens(x, q=1.0), plan).coeffs
+    minus = pb.deposit_charge(_ens(x, q=-1.0), plan).coeffs
+    assert np.array_equal(plus + minus, np.zeros_like(plus))
+
+
+def test_gather_rejects_broken_symmetry():
+    plan = pb.make_plan(8, 2 * np.pi, 1e-7)
+    rng = np.random.default_rng(32)
+    f = pb.FourierField(8, plan.L, np.fft.fftshift(np.fft.fftn(rng.standard_normal((8,) * 3)))
+                        / 8 ** 3)
+    f.coeffs[5, 4, 4] += 1.0
+    with pytest.raises(pb.FieldSymmetryError):
+        pb.gather_efield(f, f, f, _ens(rng.random((5, 3)) * plan.L), plan)
+
+
+def test_forces_match_direct_pipeline():
+    # test_pif.py:258-278: eps = 1e-12 NUFFT pipeline vs direct sums <= 1e-10
+    plan = pb.make_plan(8, 2 * np.pi, 1e-12)
+    rng = np.random.default_rng(34)
+    x = rng.random((100, 3)) * plan.L
+    q = -plan.L ** 3 / 100
+    ens = _ens(x, q=q, m=-q)
+    rho = pb.deposit_charge(ens, plan)
+    E_fast = pb.gather_efield(*pb.poisson_efield(rho), ens, plan)
+    o = oracle()
+    rho_d = o.direct_type1(o.make_plan(8, 2 * np.pi, 1e-12), x, np.full(100, q)) / plan.L ** 3
+    rho_d[4, 4, 4] = 0.0
+    Ed = np.stack([o.direct_type2(o.make_plan(8, 2 * np.pi, 1e-12), c, x).real
+                   for c in o.poisson_efield(rho_d, plan.L)], axis=1)
+    assert np.max(np.abs(E_fast - Ed)) <= 1e-10 * np.max(np.abs(Ed))
+
+
+def test_self_force_is_zero_net():
+    # adjoint deposit/gather (test_pif.py:281-294)
+    plan = pb.make_plan(8, 2 * np.pi, 1e-3)
+    rng = np.random.default_rng(35)
+    x = rng.random((500, 3)) * plan.L
+    q = -plan.L ** 3 / 500
+    ens = _ens(x, q=q, m=-q)
+    E = pb.gather_efield(*pb.poisson_efield(pb.deposit_charge(ens, plan)), ens, plan)
+    assert np.max(np.abs(q * E.sum(axis=0))) <= 1e-12 * abs(q) * np.max(np.abs(E)) * 500
+
+
+def test_boris_properties():
+    L = 2 * np.pi
+    ens = _ens([[1.0, 2.0, 3.0]], v=[[0.5, -0.25, 1.0]])
+    x0, v0 = ens.x.copy(), ens.v.copy()
+    pb.boris_push(ens, np.zeros((1, 3)), pb.ExternalFieldsSpec(L=L), 0.125, L)
+    assert np.array_equal(ens.v, v0)
+    assert np.allclose(ens.x, np.mod(x0 + 0.125 * v0, L), atol=0, rtol=1e-15)
+    ens = _ens([[0.0, 0.0, 0.0]], q=1.0, m=1.0)
+    pb.boris_push(ens, np.array([[1.0, 0.0, 0.0]]), pb.ExternalFieldsSpec(L=10.0), 0.1, 10.0)
+    assert ens.v[0, 0] == 0.1 and ens.v[0, 1] == 0.0
+
+
+def test_neutral_lattice_is_stationary():
+    plan = pb.make_plan(4, 2 * np.pi, 1e-7)
+    g = (np.arange(8) + 0.5) * (plan.L / 8)
+    X, Y, Z = np.meshgrid(g, g, g, indexing="ij")
+    x = np.stack([X.ravel(), Y.ravel(), Z.ravel()], 1)
+    q = -plan.L ** 3 / x.shape[0]
+    state = pb.StepState(ensemble=_ens(x, q=q, m=-q), plan=plan,
+                         externals=pb.ExternalFieldsSpec(L=plan.L), dt=0.05)
+    pb.pif_step(state)
+    assert np.max(np.abs(state.ensemble.x - x)) <= 1e-10
+
+
+def test_pif_step_equals_stage_composition():
+    # test_pif.py:236-255; atomic spreading sums in a different order, so
+    # equality is to rounding rather than to the bit
+    plan = pb.make_plan(8, 2 * np.pi, 1e-7)
+    rng = np.random.default_rng(33)
+    x = rng.random((64, 3)) * plan.L
+    v = rng.standard_normal((64, 3))
+    q = -plan.L ** 3 / 64
+    a = _ens(x.copy(), v=v.copy(), q=q, m=-q)
+    b = _ens(x.copy(), v=v.copy(), q=q, m=-q)
+    ext = pb.ExternalFieldsSpec(L=plan.L)
+    pb.pif_step(pb.StepState(ensemble=a, plan=plan, externals=ext, dt=0.05))
+    rho = pb.deposit_charge(b, plan)
+    E = pb.gather_efield(*pb.poisson_efield(rho), b, plan)
+    pb.boris_push(b, E, ext, 0.05, plan.L)
+    assert np.max(np.abs(a.x - b.x)) <= 1e-13 * plan.L
+    assert rel_max(a.v, b.v) <= 1e-12
+
+
+# ---------------------------------------------------------------------------
+# BASELINE config 1 (Landau / Penning 16^3, 65,536 particles) vs reference
+# ---------------------------------------------------------------------------
+
+def _config1(kind, dt=0.05, steps=20):
+    mk = pb.landau_spec if kind == "landau" else pb.penning_spec
+    spec = mk(N=16, ppm=16, dt=dt, steps=steps, seed=0)
+    ens = pb.sample_landau(spec, 0) if kind == "landau" else pb.sample_penning(spec, 0)
+    return spec, ens
+
+
+@pytest.mark.parametrize("kind", ["landau", "penning"])
+def test_config1_rho_and_E_match_reference(kind):
+    spec, ens = _config1(kind)
+    plan = pb.make_plan(spec.N, spec.L, 1e-7)
+    rho = pb.deposit_charge(ens, plan)
+    assert rel_l2(rho.coeffs, CFG[f"{kind}_rho0"]) <= CONTRACT
+    assert rel_l2(rho.coeffs, CFG[f"{kind}_rho0"]) <= TIGHT
+    E = pb.gather_efield(*pb.poisson_efield(rho), ens, plan)
+    sel = np.arange(0, ens.count, 16)
+    assert rel_l2(E[sel], CFG[f"{kind}_E0_sel"]) <= CONTRACT
+    assert rel_l2(E[sel], CFG[f"{kind}_E0_sel"]) <= TIGHT
+    assert np.linalg.norm(E) == pytest.approx(float(CFG[f"{kind}_E0_norm"][0]), rel=TIGHT)
+    pb.boris_push(ens, E, spec.externals(), spec.dt, spec.L)
+    assert rel_l2(ens.v[sel], CFG[f"{kind}_v1_sel"]) <= TIGHT
+
+
+def _trace(res):
+    cols = ("step", "t", "field_energy", "kinetic_energy", "total_energy", "px", "py", "pz",
+            "total_charge")
+    return np.array([[getattr(r, c) for c in cols] for r in [res["initial"]] + res["records"]])
+
+
+@pytest.mark.parametrize("kind,dt,tag", [("landau", 0.05, ""), ("landau", 0.003125, "_slow"),
+                                         ("penning", 0.05, "")])
+def test_serial_trace_matches_reference(kind, dt, tag):
+    spec, _ = _config1(kind, dt)
+    res = pb.spawn_spmd(1, lambda ctx: pb.run_serial(pb.RunSetup(spec=spec, eps=1e-7), ctx))[0]
+    got, ref = _trace(res), CFG[f"{kind}{tag}_trace"]
+    assert got.shape == ref.shape
+    assert np.array_equal(got[:, 0], ref[:, 0]) and np.array_equal(got[:, 1], ref[:, 1])
+    for col in (2, 3, 4):
+        err = np.max(np.abs(got[:, col] - ref[:, col]) / np.abs(ref[:, col]))
+        assert err <= TRACE and err <= 1e-10, (col, err)
+    assert np.all(got[:, 8] == ref[:, 8])     # total charge, exact
+    scale = np.max(np.abs(ref[:, 5:8])) + abs(spec.Q_e) * 1e-12
+    assert np.max(np.abs(got[:, 5:8] - ref[:, 5:8])) <= 1e-8 * scale
+
+
+def test_pd_two_ranks_matches_reference_and_logs_allreduce_only():
+    spec, _ = _config1("landau")
+    log = pb.CallLog()
+    setup = pb.RunSetup(spec=spec, eps=1e-7)
+    res = pb.spawn_spmd(2, lambda ctx: pb.run_particle_decomposition(setup, ctx), call_log=log)
+    got, ref = _trace(res[0]), CFG["landau_pd2_trace"]
+    for col in (2, 3, 4):
+        assert np.max(np.abs(got[:, col] - ref[:, col]) / np.abs(ref[:, col])) <= 1e-10
+    assert res[1]["records"] is None
+    assert log.primitives() == {"allreduce"}
+    assert len(log.records) == 2 * (spec.steps + 1)   # ONE allreduce per step and rank
+
+
+def test_damping_rate_matches_reference_fit():
+    d = golden("damping.npz")
+    spec = pb.landau_spec(N=16, ppm=10, dt=0.05, steps=200, seed=0)
+    res = pb.spawn_spmd(1, lambda ctx: pb.run_serial(pb.RunSetup(spec=spec, eps=1e-7), ctx))[0]
+    t = np.array([r.t for r in res["records"]])
+    w = np.array([r.field_energy for r in res["records"]])
+    assert np.array_equal(t, d["damp_t"])
+    assert np.max(np.abs(w - d["damp_w"]) / d["damp_w"]) <= TRACE
+    gamma = pb.fit_damping_rate(t, w)
+    assert gamma == pytest.approx(float(d["damp_gamma"][0]), rel=1e-6)
+
+
+# ---------------------------------------------------------------------------
+# window widths / paths: fused DMMA kernels (w <= 8) and the generic path
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("eps", [1e-2, 1e-3, 1e-5, 1e-6, 1e-7, 1e-9, 1e-12, 1e-15])
+def test_all_window_widths_match_oracle(eps):
+    o = oracle()
+    plan = pb.make_plan(10, 4 * np.pi, eps)
+    op = o.make_plan(10, 4 * np.pi, eps)
+    rng = np.random.default_rng(int(-np.log10(eps)))
+    x = rng.random((3000, 3)) * plan.L
+    x[:8] = (np.arange(8)[:, None] * plan.h) % plan.L      # exactly on grid points
+    x[8] = [plan.L - 1e-13, 1e-14, 0.5 * plan.L]           # at the periodic seam
+    q = rng.standard_normal(3000)
+    got = pb.type1(plan, x, q).coeffs
+    ref = o.type1(op, x, q)
+    assert rel_l2(got, ref) <= TIGHT
+    herm = [np.fft.fftshift(np.fft.fftn(rng.standard_normal((10,) * 3))) / 1000 for _ in range(3)]
+    E = nufft.gather3_real(plan, herm, x)
+    assert rel_l2(E, o.gather3_real(op, herm, x)) <= TIGHT
+
+
+def test_clustered_penning_cells():
+    # heavy cells (thousands of particles in one stencil cell) and empty ones
+    o = oracle()
+    plan = pb.make_plan(16, 25.0, 1e-7)
+    op = o.make_plan(16, 25.0, 1e-7)
+    rng = np.random.default_rng(7)
+    x = np.concatenate([12.5 + 0.01 * rng.standard_normal((20000, 3)),
+                        rng.random((2000, 3)) * 25.0])
+    q = np.full(x.shape[0], -0.1)
+    assert rel_l2(pb.type1(plan, x, q).coeffs, o.type1(op, x, q)) <= TIGHT
+
+
+# ---------------------------------------------------------------------------
+# size-independent properties at benchmark sizes (64^3 modes, 2^24 particles)
+# ---------------------------------------------------------------------------
+
+@pytest.fixture(scope="module")
+def big(cuda):
+    torch = cuda
+    from paper_2605_10729_b200.engine import PifEngine
+    from paper_2605_10729_b200.samplers import sample_device
+    spec = pb.landau_spec(N=64, ppm=64, dt=0.003125)
+    M = spec.num_particles                        # 2^24
+    plan = pb.make_plan(64, spec.L, 1e-7)
+    x, v, ids = sample_device(spec, (0, M), "cuda")
+    q, m = spec.Q_e / M, abs(spec.Q_e) / M
+    eng = PifEngine(plan, M, "cuda", q=q, m=m, externals=spec.externals(), dt=spec.dt)
+    eng.load(x, v, ids)
+    return dict(torch=torch, spec=spec, plan=plan, x=x, v=v, ids=ids, eng=eng, q=q, m=m)
+
+
+def test_binning_sorts_by_stencil_cell(big):
+    torch = big["torch"]
+    eng, plan = big["eng"], big["plan"]
+    soa = eng.parts.soa[:, :eng.count]
+    n, w, h = plan.n_up, plan.window.w, plan.h
+    keys = []
+    for d in range(3):
+        c = soa[d] / h
+        keys.append(torch.remainder(torch.ceil(c - 0.5 * w).long(), n))
+    key = (keys[0] * n + keys[1]) * n + keys[2]
+    assert bool((key[1:] >= key[:-1]).all())
+    assert torch.equal(torch.sort(eng.parts.ids[eng.parts.cur][:eng.count])[0], big["ids"])
+
+
+def test_deposit_is_permutation_invariant_and_linear(big):
+    torch = big["torch"]
+    from paper_2605_10729_b200.engine import PifEngine
+    eng, plan, q, m = big["eng"], big["plan"], big["q"], big["m"]
+    eng.deposit()
+    a = eng.raw.clone()
+    M = eng.count
+    perm = torch.randperm(M, device="cuda")
+    e2 = PifEngine(plan, M, "cuda", q=q, m=m, externals=big["spec"].externals(), dt=0.1)
+    e2.load(big["x"][perm], big["v"][perm], big["ids"][perm])
+    e2.deposit()
+    assert float((e2.raw - a).norm() / a.norm()) <= 1e-13
+    half = M // 2
+    parts = []
+    for sl in (slice(0, half), slice(half, M)):
+        e3 = PifEngine(plan, sl.stop - sl.start, "cuda", q=q, m=m,
+                       externals=big["spec"].externals(), dt=0.1)
+        e3.load(big["x"][sl], big["v"][sl], big["ids"][sl])
+        e3.deposit()
+        parts.append(e3.raw.clone())
+    assert float((parts[0] + parts[1] - a).norm() / a.norm()) <= 1e-13
+
+
+def test_charge_and_momentum_conservation_at_scale(big):
+    torch = big["torch"]
+    eng, plan = big["eng"], big["plan"]
+    # raw type-1 at k = 0 is the total charge (to the NUFFT tolerance)
+    eng.deposit()
+    N = plan.N
+    raw = torch.view_as_complex(eng.raw.view(N, N, N, 2))
+    Q = big["q"] * eng.count
+    assert abs(complex(raw[N // 2, N // 2, N // 2]) - Q) <= 10 * plan.eps * abs(Q)
+    table = eng.run(3)
+    host = table.cpu().numpy()
+    p = host[:, 2:5] * big["m"]
+    assert np.max(np.abs(p - p[0])) <= 1e-10 * big["m"] * eng.count
+    assert np.all(host[:, 6] <= 1e-10)         # Hermitian guard clean every step
+
+
+def test_gather_self_force_at_scale(big):
+    torch = big["torch"]
+    eng, plan = big["eng"], big["plan"]
+    eng.deposit()
+    eng.solve_fields()
+    M = eng.count
+    E = torch.empty((M, 3), dtype=torch.float64, device="cuda")
+    from paper_2605_10729_b200 import _native
+    import ctypes
+    cur = eng._soa()
+    _native.call("pif_interp_sorted", eng.handle, ctypes.byref(cur), E.data_ptr(),
+                 _native.stream_handle())
+    net = E.sum(dim=0).abs().max().item()
+    assert net <= 1e-10 * E.abs().max().item() * M

@@ -1,0 +1,67 @@
+"""The C ABI library: loads without a GPU, exports every symbol the header
+declares, and the ctypes signature table covers them all.  CPU only."""
+
+import os
+import re
+import subprocess
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "pif_b200.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char \*)\s*(pif_\w+)\s*\(", text,
+                                 re.M)))
+
+
+def test_header_declares_the_hot_path():
+    syms = declared_symbols()
+    for s in ("pif_plan_create", "pif_bin_keys", "pif_bin_scatter", "pif_spread_sorted",
+              "pif_grid_to_modes", "pif_solve_fields", "pif_interp_push", "pif_interp_sorted"):
+        assert s in syms
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    from paper_2605_10729_b200 import _native
+    lib = _native.load()
+    assert lib.pif_abi_version() == 1
+    out = subprocess.run(["nm", "-D", "--defined-only", _native.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (pif_\w+)", out))
+    missing = [s for s in declared_symbols() if s not in exported]
+    assert not missing, missing
+
+
+def test_ctypes_table_matches_header():
+    from paper_2605_10729_b200 import _native
+    assert sorted(_native.SIGNATURES) == declared_symbols()
+
+
+def test_library_is_sm100a():
+    from paper_2605_10729_b200 import _native
+    out = subprocess.run(["cuobjdump", "--list-elf", _native.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_hot_kernels_use_fp64_tensor_cores():
+    """The fused spread / gather kernels are DMMA (fp64 mma.sync) kernels."""
+    from paper_2605_10729_b200 import _native
+    out = subprocess.run(["cuobjdump", "-sass", _native.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "DMMA.8x8x4" in out
+    assert "REDG.E.ADD.F64" in out
+
+
+def test_errors_map_to_python_exceptions():
+    import ctypes
+
+    import pytest
+
+    from paper_2605_10729_b200 import _native
+    lib = _native.load()
+    h = ctypes.c_void_p()
+    with pytest.raises(ValueError):
+        _native.check(lib.pif_plan_create(None, 0, ctypes.byref(h)), "pif_plan_create")
