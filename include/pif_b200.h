@@ -76,6 +76,10 @@ int pif_plan_create(const pif_plan_desc_t *desc, int device, pif_plan_t *out);
 int pif_plan_destroy(pif_plan_t plan);
 /* Bytes of device memory owned by the plan. */
 int64_t pif_plan_device_bytes(pif_plan_t plan);
+/* Host-only: the interior ES-weight polynomials a plan builds for window w
+ * (es_fast.cuh): max abs error vs the exact window on 4001 points, and the mask
+ * of weights that fall back to the exact formula.  w in [2, 8]. */
+int pif_es_poly_info(int w, double beta, double *max_err, int *exact_mask);
 
 /* ---- binning (new; the reference spreads in particle order, _kernels.py:73) -
  * pif_bin_keys: per-particle ES-stencil cell key ((i0x*n + i0y)*n + i0z, each

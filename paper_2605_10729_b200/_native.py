@@ -53,6 +53,7 @@ SIGNATURES = {
     "pif_plan_create": ([ctypes.POINTER(pif_plan_desc_t), _I, ctypes.POINTER(_P)], _I),
     "pif_plan_destroy": ([_P], _I),
     "pif_plan_device_bytes": ([_P], _I64),
+    "pif_es_poly_info": ([_I, _D, _D3, ctypes.POINTER(ctypes.c_int)], _I),
     "pif_wrap_points": ([_P, _P, _P, _P, _I64, _P], _I),
     "pif_bin_keys": ([_P, _SOA, _P, _P, _P], _I),
     "pif_bin_scatter": ([_P, _SOA, _SOA, _P, _P, _I, _P], _I),

@@ -86,6 +86,65 @@ int ensure_complex(Plan &p) {
     return PIF_OK;
 }
 
+// Chebyshev interpolation (extended precision) of weight a as a function of
+// u = 2f - 1, converted to monomials; each polynomial is verified on a fine grid
+// and replaced by the exact formula (exact_mask) if it misses 4e-15.
+void build_es_poly(int w, double beta, EsPolyHost *P, double *max_err) {
+    std::memset(P, 0, sizeof(*P));
+    double worst = 0.0;
+    const int D = kEsDegHost;
+    const long double pi = 3.141592653589793238462643383279502884L;
+    const long double B = (long double)beta;
+    auto phi = [&](long double t) {
+        long double u = 1.0L - t * t;
+        if (u < 0) u = 0;
+        return expl(B * (sqrtl(u) - 1.0L));
+    };
+    for (int a = 1; a + 1 < w && a <= 6; ++a) {
+        long double y[kEsDegHost + 1], cheb[kEsDegHost + 1];
+        for (int k = 0; k <= D; ++k) {
+            const long double un = cosl(pi * (k + 0.5L) / (D + 1));
+            const long double f = 0.5L * (un + 1.0L);
+            y[k] = phi(1.0L - (2.0L / w) * (a + f));
+        }
+        for (int j = 0; j <= D; ++j) {
+            long double s = 0;
+            for (int k = 0; k <= D; ++k) s += y[k] * cosl(pi * j * (k + 0.5L) / (D + 1));
+            cheb[j] = (2.0L / (D + 1)) * s;
+        }
+        cheb[0] *= 0.5L;
+        long double mono[kEsDegHost + 1] = {0}, t0[kEsDegHost + 1] = {0},
+                    t1[kEsDegHost + 1] = {0}, t2[kEsDegHost + 1];
+        t0[0] = 1.0L;
+        t1[1] = 1.0L;
+        for (int k = 0; k <= D; ++k) mono[k] += cheb[0] * t0[k] + cheb[1] * t1[k];
+        for (int j = 2; j <= D; ++j) {
+            for (int k = 0; k <= D; ++k) t2[k] = -t0[k] + (k ? 2.0L * t1[k - 1] : 0.0L);
+            for (int k = 0; k <= D; ++k) {
+                mono[k] += cheb[j] * t2[k];
+                t0[k] = t1[k];
+                t1[k] = t2[k];
+            }
+        }
+        for (int k = 0; k <= D; ++k) P->c[a - 1][k] = (double)mono[k];
+        double err = 0.0;
+        for (int i = 0; i <= 4000; ++i) {
+            const double f = i / 4000.0 * (1.0 - 1e-12);
+            const double u = 2.0 * f - 1.0;
+            double p = P->c[a - 1][D];
+            for (int k = D - 1; k >= 0; --k) p = std::fma(p, u, P->c[a - 1][k]);
+            const double e = std::fabs(p - (double)phi(1.0L - (2.0L / w) * (a + (long double)f)));
+            if (e > err) err = e;
+        }
+        if (err > 4e-15) {
+            P->exact_mask |= 1 << (a - 1);
+        } else if (err > worst) {
+            worst = err;
+        }
+    }
+    if (max_err) *max_err = worst;
+}
+
 }  // namespace pif
 
 using pif::Plan;
@@ -130,6 +189,7 @@ int pif_plan_create(const pif_plan_desc_t *d, int device, pif_plan_t *out) {
     const int64_t N3 = (int64_t)p.N * p.N * p.N;
     cudaDeviceGetAttribute(&p.sm_count, cudaDevAttrMultiProcessorCount, device);
     p.partial_blocks = p.sm_count * 32;
+    pif::build_es_poly(p.w, p.beta, &p.poly, &p.poly_err);
     int rc = PIF_OK;
 #define TRY(x)                    \
     do {                          \
@@ -221,6 +281,16 @@ int pif_plan_destroy(pif_plan_t plan) {
 }
 
 int64_t pif_plan_device_bytes(pif_plan_t plan) { return plan ? plan->p.bytes : 0; }
+
+int pif_es_poly_info(int w, double beta, double *max_err, int *exact_mask) {
+    if (w < 2 || w > pif::kMaxFastW || !(beta > 0)) return pif::bad("w must be in [2, 8]");
+    pif::EsPolyHost P;
+    double e = 0.0;
+    pif::build_es_poly(w, beta, &P, &e);
+    if (max_err) *max_err = e;
+    if (exact_mask) *exact_mask = P.exact_mask;
+    return PIF_OK;
+}
 
 #define PLAN_CHECK()                                          \
     if (!plan) return pif::bad("null plan");                  \

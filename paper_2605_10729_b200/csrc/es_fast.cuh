@@ -63,3 +63,89 @@ __device__ __forceinline__ double es_weight_fast(double c, double i, double inv_
 }
 
 }  // namespace pif
+
+namespace pif {
+
+// Interior window weights as polynomials.  For a coordinate c (grid units) with
+// x = c - w/2, i0 = ceil(x) and f = i0 - x in [0, 1) (both steps exact), weight a
+// is phi(1 - (2/w)(a + f)).  For 1 <= a <= w-2 this is analytic on f in [0, 1]
+// (the sqrt branch points of phi sit at a + f = 0 and a + f = w), so it is
+// evaluated as a degree-kEsDeg polynomial in u = 2f - 1 (Horner, coefficients
+// from Chebyshev interpolation in extended precision at plan creation,
+// build_es_poly in capi.cu; max error < 4e-15 absolute, checked there).  The
+// two edge weights keep the exact formula.
+constexpr int kEsDeg = 14;
+
+struct EsPoly {
+    double c[kMaxFastW - 2][kEsDeg + 1];   // [a - 1][power]
+    int exact_mask;                        // bit a-1 set: evaluate weight a exactly
+};
+
+template <int W>
+__device__ __forceinline__ void es_axis_weights(double c, double beta, const EsPoly &P,
+                                                const double *tab, double (&wt)[W]) {
+    constexpr double inv_half = 2.0 / W;
+    const double i0 = stencil_start(c, W);
+    wt[0] = es_weight_fast(c, i0, inv_half, beta, tab);
+    if (W > 1) wt[W - 1] = es_weight_fast(c, i0 + (double)(W - 1), inv_half, beta, tab);
+    const double f = i0 - __dsub_rn(c, 0.5 * W);
+    const double u = fma(2.0, f, -1.0);
+#pragma unroll
+    for (int a = 1; a + 1 < W; ++a) {
+        if (P.exact_mask & (1 << (a - 1))) {
+            wt[a] = es_weight_fast(c, i0 + (double)a, inv_half, beta, tab);
+        } else {
+            double p = P.c[a - 1][kEsDeg];
+#pragma unroll
+            for (int k = kEsDeg - 1; k >= 0; --k) p = fma(p, u, P.c[a - 1][k]);
+            wt[a] = p;
+        }
+    }
+}
+
+}  // namespace pif
+
+namespace pif {
+
+// All three axes at once: the 3*(w-2) interior Horner chains advance together
+// (power-outer loop) so a warp has 18 independent FMAs in flight per step.
+template <int W>
+__device__ __forceinline__ void es_xyz_weights(const double (&c)[3], double beta, const EsPoly &P,
+                                               const double *tab, double (&wt)[3][W]) {
+    constexpr double inv_half = 2.0 / W;
+    constexpr int NI = W > 2 ? W - 2 : 0;
+    double u[3], i0[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        i0[d] = stencil_start(c[d], W);
+        u[d] = fma(2.0, i0[d] - __dsub_rn(c[d], 0.5 * W), -1.0);
+    }
+    if (NI > 0) {
+        double p[3][NI > 0 ? NI : 1];
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+            for (int a = 0; a < NI; ++a) p[d][a] = P.c[a][kEsDeg];
+#pragma unroll
+        for (int k = kEsDeg - 1; k >= 0; --k)
+#pragma unroll
+            for (int d = 0; d < 3; ++d)
+#pragma unroll
+                for (int a = 0; a < NI; ++a) p[d][a] = fma(p[d][a], u[d], P.c[a][k]);
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+            for (int a = 0; a < NI; ++a) wt[d][a + 1] = p[d][a];
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        wt[d][0] = es_weight_fast(c[d], i0[d], inv_half, beta, tab);
+        if (W > 1) wt[d][W - 1] = es_weight_fast(c[d], i0[d] + (double)(W - 1), inv_half, beta, tab);
+#pragma unroll
+        for (int a = 1; a + 1 < W; ++a)
+            if (P.exact_mask & (1 << (a - 1)))
+                wt[d][a] = es_weight_fast(c[d], i0[d] + (double)a, inv_half, beta, tab);
+    }
+}
+
+}  // namespace pif

@@ -14,6 +14,8 @@
 // (gather) exactly one plane.  Window weights come from es_fast.cuh.
 #include <cub/cub.cuh>
 
+#include <cstring>
+
 #include "pif_internal.cuh"
 #include "es_fast.cuh"
 
@@ -113,31 +115,38 @@ __device__ __forceinline__ void chunk_zero(WarpChunk &st, int lane) {
     __syncwarp();
 }
 
-// Window weights of this lane's particle (lane < cnt): c = x/h, i0 = ceil(c - w/2),
-// w weights per axis (_kernels.py:11-28), x row scaled by the strength s.
-template <int W>
-__device__ __forceinline__ void chunk_weights(WarpChunk &st, const double *tab, int lane, int cnt,
-                                              double x, double y, double z, double s, bool scale,
-                                              double h, double beta) {
-    constexpr double inv_half = 2.0 / W;
+// Window weights of this lane's particle (lane < cnt): c = x/h and the w
+// weights per axis (_kernels.py:11-28; interior ones by polynomial,
+// es_fast.cuh), x row scaled by the strength s.
+// XYZ: advance the three axes' polynomial chains together (more ILP, more
+// registers) — used by the low-occupancy gather kernel; the spread kernel runs
+// enough warps to hide the per-axis chains and keeps its registers low.
+template <int W, bool XYZ>
+__device__ __forceinline__ void chunk_weights(WarpChunk &st, const double *tab, const EsPoly &P,
+                                              int lane, int cnt, double x, double y, double z,
+                                              double s, bool scale, double h, double beta) {
     if (lane < cnt) {
-        const double xyz[3] = {x, y, z};
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            const double c = axis_coord(xyz[d], h);
-            const double i0 = stencil_start(c, W);
+        if (XYZ) {
+            const double c[3] = {axis_coord(x, h), axis_coord(y, h), axis_coord(z, h)};
+            double wt[3][W];
+            es_xyz_weights<W>(c, beta, P, tab, wt);
 #pragma unroll
             for (int a = 0; a < W; ++a) {
-                double v = es_weight_fast(c, i0 + (double)a, inv_half, beta, tab);
-                if (d == 0) {
-                    if (scale) v = __dmul_rn(s, v);   // sa = s * wx[a] (_kernels.py:81)
-                    st.wx[a][lane] = v;
-                } else if (d == 1) {
-                    st.wy[lane][a] = v;
-                } else {
-                    st.wz[lane][a] = v;
-                }
+                st.wx[a][lane] = scale ? __dmul_rn(s, wt[0][a]) : wt[0][a];
+                st.wy[lane][a] = wt[1][a];
+                st.wz[lane][a] = wt[2][a];
             }
+        } else {
+            double wt[W];
+            es_axis_weights<W>(axis_coord(x, h), beta, P, tab, wt);
+#pragma unroll
+            for (int a = 0; a < W; ++a) st.wx[a][lane] = scale ? __dmul_rn(s, wt[a]) : wt[a];
+            es_axis_weights<W>(axis_coord(y, h), beta, P, tab, wt);
+#pragma unroll
+            for (int a = 0; a < W; ++a) st.wy[lane][a] = wt[a];
+            es_axis_weights<W>(axis_coord(z, h), beta, P, tab, wt);
+#pragma unroll
+            for (int a = 0; a < W; ++a) st.wz[lane][a] = wt[a];
         }
     }
     __syncwarp();
@@ -182,7 +191,8 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
                   const double *__restrict__ pz, const int64_t *__restrict__ pid,
                   const double *__restrict__ strengths, double q,
                   const int32_t *__restrict__ cell_start, double *__restrict__ grid, int n,
-                  int seg, int nseg, double h, double beta, unsigned int *work, int nitems) {
+                  int seg, int nseg, double h, double beta, const EsPoly poly, unsigned int *work,
+                  int nitems) {
     __shared__ WarpChunk stage[kWarpsPerBlock];
     __shared__ double tab[32];
     if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
@@ -229,7 +239,7 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
                 nz = pz[i];
                 if (strengths) ns = strengths[pid[i]];
             }
-            chunk_weights<W>(st, tab, lane, cnt, cx, cy, cz, cs, true, h, beta);
+            chunk_weights<W, false>(st, tab, poly, lane, cnt, cx, cy, cz, cs, true, h, beta);
             int j = 0;
             while (j < cnt) {
                 const int gp = pos + j;
@@ -411,9 +421,10 @@ template <int W, bool PUSH>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, PIF_INTERP_MINB)
 interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ cell_start,
                   const double4 *__restrict__ field, int seg, int nseg, double beta,
-                  PushParams pp, int32_t *__restrict__ key, int32_t *__restrict__ rank,
-                  int32_t *__restrict__ count, double *__restrict__ partials,
-                  double *__restrict__ E_out, unsigned int *work, int nitems) {
+                  const EsPoly poly, PushParams pp, int32_t *__restrict__ key,
+                  int32_t *__restrict__ rank, int32_t *__restrict__ count,
+                  double *__restrict__ partials, double *__restrict__ E_out, unsigned int *work,
+                  int nitems) {
     __shared__ WarpChunk stage[kWarpsPerBlock];
     __shared__ double tab[32];
     if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
@@ -464,7 +475,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ cell_start,
                 nx = P.x[i]; ny = P.y[i]; nz = P.z[i];
                 if (PUSH) { nvx = P.vx[i]; nvy = P.vy[i]; nvz = P.vz[i]; }
             }
-            chunk_weights<W>(st, tab, lane, cnt, x0, y0, z0, 1.0, false, h, beta);
+            chunk_weights<W, true>(st, tab, poly, lane, cnt, x0, y0, z0, 1.0, false, h, beta);
             int j = 0;
             while (j < cnt) {
                 const int gp = pos + j;
@@ -754,8 +765,17 @@ int launch_bin_scatter(Plan &p, const pif_soa_t &src, pif_soa_t &dst, const int3
                      "reset cell counts");
 }
 
+static EsPoly device_poly(const Plan &p) {
+    static_assert(sizeof(EsPoly) == sizeof(EsPolyHost), "EsPoly layout");
+    static_assert(kEsDeg == kEsDegHost, "EsPoly degree");
+    EsPoly e;
+    std::memcpy(&e, &p.poly, sizeof(e));
+    return e;
+}
+
 int launch_spread(Plan &p, const pif_soa_t &P, const double *strengths, double q,
                   cudaStream_t s) {
+    const EsPoly poly = device_poly(p);
     cudaError_t e = cudaMemsetAsync(p.grid, 0, sizeof(double) * p.n3, s);
     if (e != cudaSuccess) return fail_cuda(e, "zero grid");
     if (P.count == 0) return PIF_OK;
@@ -770,7 +790,7 @@ int launch_spread(Plan &p, const pif_soa_t &P, const double *strengths, double q
         auto k = spread_mma_kernel<W>;                                                      \
         int blocks = persistent_blocks(k, threads, 0, p.sm_count);                           \
         k<<<blocks, threads, 0, s>>>(P.x, P.y, P.z, P.id, strengths, q, p.cell_start, p.grid, \
-                                     p.n, p.seg, nseg, p.h, p.beta, p.work, nitems);         \
+                                     p.n, p.seg, nseg, p.h, p.beta, poly, p.work, nitems);   \
         break;                                                                               \
     }
         switch (p.w) {
@@ -801,6 +821,7 @@ int launch_interp(Plan &p, pif_soa_t &P, bool push, double half, double dt, cons
         return PIF_ERR_STATE;
     }
     PushParams pp = make_push(p, half, dt, tq, sq, has_b, e_kind);
+    const EsPoly poly = device_poly(p);
     const double4 *field = reinterpret_cast<const double4 *>(p.field);
     cudaError_t e;
     int blocks = 1;
@@ -816,14 +837,14 @@ int launch_interp(Plan &p, pif_soa_t &P, bool push, double half, double dt, cons
             auto k = interp_mma_kernel<W, true>;                                             \
             blocks = persistent_blocks(k, threads, 0, p.sm_count);                            \
             if (blocks > p.partial_blocks) blocks = p.partial_blocks;                         \
-            k<<<blocks, threads, 0, s>>>(P, p.cell_start, field, p.seg, nseg, p.beta, pp, key, \
-                                         rank, p.cell_count, p.partials, E_out, p.work,        \
+            k<<<blocks, threads, 0, s>>>(P, p.cell_start, field, p.seg, nseg, p.beta, poly, pp, \
+                                         key, rank, p.cell_count, p.partials, E_out, p.work,   \
                                          nitems);                                             \
         } else {                                                                              \
             auto k = interp_mma_kernel<W, false>;                                            \
             blocks = persistent_blocks(k, threads, 0, p.sm_count);                            \
-            k<<<blocks, threads, 0, s>>>(P, p.cell_start, field, p.seg, nseg, p.beta, pp, key, \
-                                         rank, p.cell_count, p.partials, E_out, p.work,        \
+            k<<<blocks, threads, 0, s>>>(P, p.cell_start, field, p.seg, nseg, p.beta, poly, pp, \
+                                         key, rank, p.cell_count, p.partials, E_out, p.work,   \
                                          nitems);                                             \
         }                                                                                     \
         break;                                                                                \

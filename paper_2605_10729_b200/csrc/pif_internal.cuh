@@ -19,6 +19,14 @@ constexpr int kSub = 8;            // particles per warp sub-batch (fast kernels
 constexpr int kWarpsPerBlock = 4;  // fast kernels: one work item per warp
 constexpr int kDiagSlots = 6;
 
+// polynomial coefficients for the interior window weights (es_fast.cuh)
+constexpr int kEsDegHost = 14;
+struct EsPolyHost {
+    double c[6][kEsDegHost + 1];
+    int exact_mask;
+};
+void build_es_poly(int w, double beta, EsPolyHost *out, double *max_err);
+
 struct Plan {
     int N = 0, n = 0, w = 0, device = 0;
     double L = 0, eps = 0, beta = 0, h = 0, inv_L3 = 0, half_L3 = 0;
@@ -46,6 +54,8 @@ struct Plan {
     bool field_valid = false;
     int sm_count = 148;
     int64_t bytes = 0;
+    EsPolyHost poly{};              // interior weight polynomials for w <= 8
+    double poly_err = 0;            // their max abs error (checked at creation)
 };
 
 void set_error(const std::string &msg);

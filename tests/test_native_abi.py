@@ -65,3 +65,18 @@ def test_errors_map_to_python_exceptions():
     h = ctypes.c_void_p()
     with pytest.raises(ValueError):
         _native.check(lib.pif_plan_create(None, 0, ctypes.byref(h)), "pif_plan_create")
+
+
+def test_interior_weight_polynomials_are_accurate():
+    """Host-side check of the polynomial window weights every plan builds."""
+    import ctypes
+
+    from paper_2605_10729_b200 import _native
+    lib = _native.load()
+    for w in range(2, 9):
+        err = (ctypes.c_double * 3)()
+        mask = ctypes.c_int()
+        _native.check(lib.pif_es_poly_info(w, 2.30 * w, err, ctypes.byref(mask)))
+        if w >= 6:                     # eps <= 1e-5: every interior weight is a polynomial
+            assert mask.value == 0, (w, mask.value)
+        assert err[0] <= 4e-15, (w, err[0])   # polynomials in use meet the bound
