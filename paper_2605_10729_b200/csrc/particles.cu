@@ -413,6 +413,43 @@ __device__ __forceinline__ void gather_sub(WarpChunk &st, const double (&g)[8][2
     }
 }
 
+// Next-plane prefetch: all 32 lanes copy the 8 x 8 double4 block of plane z
+// into shared memory with cp.async (LDGSTS) one cell ahead of its use.
+__device__ __forceinline__ void prefetch_plane(double4 (*pf)[8], const double4 *field, int ix,
+                                               int iy, int n, int64_t z, int lane) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const int q = lane + 32 * t;              // 16-byte chunk: (a, b, half)
+        const int a = q >> 4, b = (q >> 1) & 7, hf = q & 1;
+        int xa = ix + a;
+        xa = xa >= n ? xa - n : xa;
+        int yb = iy + b;
+        yb = yb >= n ? yb - n : yb;
+        const char *src = reinterpret_cast<const char *>(field + ((int64_t)xa * n + yb) * n + z) +
+                          16 * hf;
+        const unsigned dst =
+            (unsigned)__cvta_generic_to_shared(reinterpret_cast<char *>(&pf[a][b]) + 16 * hf);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src));
+    }
+    asm volatile("cp.async.commit_group;");
+}
+
+__device__ __forceinline__ void prefetch_wait() {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+}
+
+__device__ __forceinline__ void plane_from_smem(double (&g)[8][2][3], int hh, double4 (*pf)[8],
+                                                int r) {
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+        const double4 f = pf[a][r];
+        g[a][hh][0] = f.x;
+        g[a][hh][1] = f.y;
+        g[a][hh][2] = f.z;
+    }
+}
+
 #ifndef PIF_INTERP_MINB
 #define PIF_INTERP_MINB 2
 #endif
@@ -426,16 +463,22 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ cell_start,
                   double *__restrict__ partials, double *__restrict__ E_out, unsigned int *work,
                   int nitems) {
     __shared__ WarpChunk stage[kWarpsPerBlock];
+    __shared__ double4 planes[kWarpsPerBlock][8][8];
     __shared__ double tab[32];
     if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
     __syncthreads();
     const int lane = threadIdx.x & 31;
     WarpChunk &st = stage[threadIdx.x >> 5];
+    double4 (*pf)[8] = planes[threadIdx.x >> 5];
     chunk_zero(st, lane);
     const int n = pp.n;
     const double h = pp.h;
     const int r = lane >> 2, c4 = lane & 3;
     double dg[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    // rank of the previous chunk's particle: stored one chunk later so the
+    // atomic's round trip overlaps the next chunk's work
+    int64_t rank_idx = -1;
+    int rank_val = 0;
 
     for (;;) {
         int item = 0;
@@ -446,7 +489,8 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ cell_start,
         const int ix = col / n, iy = col - ix * n;
         const int k0 = sg * seg, k1 = min(k0 + seg, n);
         const int base = col * n;
-        const int pbeg = cell_start[base + k0], pend = cell_start[base + k1];
+        const int cb = cell_start[base + k0 + min(lane, k1 - k0)];   // seg <= 31
+        const int pbeg = __shfl_sync(kFull, cb, 0), pend = __shfl_sync(kFull, cb, k1 - k0);
         if (pbeg == pend) continue;
         const int64_t yrow = (iy + r) % n;
 
@@ -465,11 +509,17 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ cell_start,
             load_plane(g, hh, field, ix, yrow, n, (k0 + ((s - k0) & 7)) % n);
         }
         int k = k0;
-        int cell_end = cell_start[base + k0 + 1];
+        int cell_end = __shfl_sync(kFull, cb, 1);
+        prefetch_wait();   // previous item's outstanding prefetch
+        prefetch_plane(pf, field, ix, iy, n, (k0 + 8) % n, lane);
 
         for (int pos = pbeg; pos < pend; pos += kChunk) {
             const int cnt = min(kChunk, pend - pos);
             const double x0 = nx, y0 = ny, z0 = nz, vx0 = nvx, vy0 = nvy, vz0 = nvz;
+            if (PUSH && rank_idx >= 0) {
+                rank[rank_idx] = rank_val;
+                rank_idx = -1;
+            }
             if (pos + kChunk + lane < pend) {   // prefetch the next chunk
                 const int i = pos + kChunk + lane;
                 nx = P.x[i]; ny = P.y[i]; nz = P.z[i];
@@ -481,13 +531,15 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ cell_start,
                 const int gp = pos + j;
                 if (gp >= cell_end) {   // next cell: plane k leaves slot k&7, plane k+8 enters
                     const int s = k & 7;
+                    prefetch_wait();
                     if (c4 == (s & 3)) {
-                        const int64_t z = (k + 8) % n;
-                        if (s >> 2) load_plane(g, 1, field, ix, yrow, n, z);
-                        else load_plane(g, 0, field, ix, yrow, n, z);
+                        if (s >> 2) plane_from_smem(g, 1, pf, r);
+                        else plane_from_smem(g, 0, pf, r);
                     }
+                    __syncwarp();
                     ++k;
-                    cell_end = cell_start[base + k + 1];
+                    prefetch_plane(pf, field, ix, iy, n, (k + 8) % n, lane);
+                    cell_end = __shfl_sync(kFull, cb, k - k0 + 1);
                     continue;
                 }
                 const int m = min(8, min(pos + cnt, cell_end) - gp);
@@ -506,7 +558,8 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ cell_start,
                     P.vx[i] = vx; P.vy[i] = vy; P.vz[i] = vz;
                     const int kk = cell_key(x, y, z, h, pp.w, n);
                     key[i] = kk;
-                    rank[i] = atomicAdd(&count[kk], 1);
+                    rank_val = atomicAdd(&count[kk], 1);
+                    rank_idx = i;
                 } else {
                     const int64_t o = 3 * P.id[i];
                     E_out[o] = E0;
@@ -517,6 +570,8 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ cell_start,
             __syncwarp();
         }
     }
+    prefetch_wait();
+    if (PUSH && rank_idx >= 0) rank[rank_idx] = rank_val;
     if (PUSH) block_diag_store(dg, partials);
 }
 
