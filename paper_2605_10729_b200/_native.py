@@ -58,6 +58,9 @@ SIGNATURES = {
     "pif_bin_keys": ([_P, _SOA, _P, _P, _P], _I),
     "pif_bin_scatter": ([_P, _SOA, _SOA, _P, _P, _I, _P], _I),
     "pif_spread_sorted": ([_P, _SOA, _P, _D, _P], _I),
+    "pif_bin_perm": ([_P, _P, _P, _I64, _P, _P], _I),
+    "pif_spread_perm": ([_P, _SOA, _P, _P, _D, _P], _I),
+    "pif_interp_push_perm": ([_P, _SOA, _P, _SOA, _D, _D, _D3, _D3, _I, _I, _P, _P, _P, _P], _I),
     "pif_grid_to_modes": ([_P, _P, _P], _I),
     "pif_solve_fields": ([_P, _P, _I, _P, _P, _P], _I),
     "pif_fields_from_modes": ([_P, _P, _P, _P, _I, _P, _P], _I),
@@ -65,6 +68,7 @@ SIGNATURES = {
     "pif_poisson": ([_P, _P, _P, _P, _P, _P], _I),
     "pif_interp_push": ([_P, _SOA, _D, _D, _D3, _D3, _I, _I, _P, _P, _P, _P], _I),
     "pif_interp_sorted": ([_P, _SOA, _P, _P], _I),
+    "pif_interp_perm": ([_P, _SOA, _P, _P, _P], _I),
     "pif_particle_diag": ([_P, _SOA, _I, _P, _P], _I),
     "pif_type1_complex": ([_P, _P, _P, _I64, _P, _P], _I),
     "pif_type2_complex": ([_P, _P, _P, _I64, _P, _P], _I),

@@ -328,7 +328,42 @@ int pif_spread_sorted(pif_plan_t plan, const pif_soa_t *sorted, const double *st
                       double q, void *stream) {
     PLAN_CHECK();
     if (!pif::soa_ok(sorted, false)) return pif::bad("invalid particle view");
-    return pif::launch_spread(p, *sorted, strengths, q, s);
+    return pif::launch_spread(p, *sorted, nullptr, strengths, q, s);
+}
+
+int pif_bin_perm(pif_plan_t plan, const int32_t *key, const int32_t *rank, int64_t M,
+                 int32_t *perm, void *stream) {
+    PLAN_CHECK();
+    if (M < 0 || M >= (int64_t)INT32_MAX || (M > 0 && (!key || !rank || !perm)))
+        return pif::bad("invalid binning arguments");
+    return pif::launch_bin_perm(p, key, rank, M, perm, s);
+}
+
+int pif_spread_perm(pif_plan_t plan, const pif_soa_t *parts, const int32_t *perm,
+                    const double *strengths, double q, void *stream) {
+    PLAN_CHECK();
+    if (!pif::soa_ok(parts, false)) return pif::bad("invalid particle view");
+    return pif::launch_spread(p, *parts, perm, strengths, q, s);
+}
+
+int pif_interp_push_perm(pif_plan_t plan, const pif_soa_t *src, const int32_t *perm,
+                         pif_soa_t *dst, double half, double dt, const double tq[3],
+                         const double sq[3], int has_b, int e_kind, int32_t *key, int32_t *rank,
+                         double *diag, void *stream) {
+    PLAN_CHECK();
+    if (!pif::soa_ok(src, true) || !dst) return pif::bad("invalid particle view");
+    pif_soa_t d = *dst;
+    d.count = src->count;
+    if (!pif::soa_ok(&d, true)) return pif::bad("invalid destination view");
+    if (src->count > 0 && (!key || !rank || !perm)) return pif::bad("missing key/rank/perm");
+    if (!diag) return pif::bad("null diag");
+    if (e_kind != PIF_EXT_NONE && e_kind != PIF_EXT_QUADRUPOLE) return pif::bad("unknown e_kind");
+    if (!(dt > 0)) return pif::bad("dt must be positive");
+    if (d.x == src->x) return pif::bad("dst must not alias src");
+    int rc = pif::launch_interp(p, *src, perm, d, true, half, dt, tq, sq, has_b, e_kind, key,
+                                rank, diag, nullptr, s);
+    dst->count = d.count;
+    return rc;
 }
 
 int pif_grid_to_modes(pif_plan_t plan, double *modes, void *stream) {
@@ -376,8 +411,8 @@ int pif_interp_push(pif_plan_t plan, pif_soa_t *sorted, double half, double dt,
     if (!diag) return pif::bad("null diag");
     if (e_kind != PIF_EXT_NONE && e_kind != PIF_EXT_QUADRUPOLE) return pif::bad("unknown e_kind");
     if (!(dt > 0)) return pif::bad("dt must be positive");
-    return pif::launch_interp(p, *sorted, true, half, dt, tq, sq, has_b, e_kind, key, rank, diag,
-                              nullptr, s);
+    return pif::launch_interp(p, *sorted, nullptr, *sorted, true, half, dt, tq, sq, has_b, e_kind,
+                              key, rank, diag, nullptr, s);
 }
 
 int pif_interp_sorted(pif_plan_t plan, const pif_soa_t *sorted, double *E_out, void *stream) {
@@ -385,8 +420,18 @@ int pif_interp_sorted(pif_plan_t plan, const pif_soa_t *sorted, double *E_out, v
     if (!pif::soa_ok(sorted, false)) return pif::bad("invalid particle view");
     if (sorted->count > 0 && !E_out) return pif::bad("null E_out");
     pif_soa_t v = *sorted;
-    return pif::launch_interp(p, v, false, 0.0, 1.0, nullptr, nullptr, 0, PIF_EXT_NONE, nullptr,
-                              nullptr, nullptr, E_out, s);
+    return pif::launch_interp(p, v, nullptr, v, false, 0.0, 1.0, nullptr, nullptr, 0, PIF_EXT_NONE,
+                              nullptr, nullptr, nullptr, E_out, s);
+}
+
+int pif_interp_perm(pif_plan_t plan, const pif_soa_t *parts, const int32_t *perm, double *E_out,
+                    void *stream) {
+    PLAN_CHECK();
+    if (!pif::soa_ok(parts, false)) return pif::bad("invalid particle view");
+    if (parts->count > 0 && (!E_out || !perm)) return pif::bad("null E_out/perm");
+    pif_soa_t v = *parts;
+    return pif::launch_interp(p, v, perm, v, false, 0.0, 1.0, nullptr, nullptr, 0, PIF_EXT_NONE,
+                              nullptr, nullptr, nullptr, E_out, s);
 }
 
 int pif_particle_diag(pif_plan_t plan, const pif_soa_t *ps, int e_kind, double *diag,

@@ -80,6 +80,15 @@ __global__ void bin_scatter_kernel(pif_soa_t src, pif_soa_t dst, const int32_t *
     }
 }
 
+// perm[start[key[j]] + rank[j]] = j: the cell-ordered view of a particle set
+__global__ void bin_perm_kernel(const int32_t *__restrict__ key, const int32_t *__restrict__ rank,
+                                const int32_t *__restrict__ start, int64_t M,
+                                int32_t *__restrict__ perm) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < M;
+         j += (int64_t)gridDim.x * blockDim.x)
+        perm[start[key[j]] + rank[j]] = (int32_t)j;
+}
+
 // ----------------------------------------------------------------------------
 // DMMA building blocks
 // ----------------------------------------------------------------------------
@@ -189,7 +198,7 @@ template <int W>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
                   const double *__restrict__ pz, const int64_t *__restrict__ pid,
-                  const double *__restrict__ strengths, double q,
+                  const int32_t *__restrict__ perm, const double *__restrict__ strengths, double q,
                   const int32_t *__restrict__ cell_start, double *__restrict__ grid, int n,
                   int seg, int nseg, double h, double beta, const EsPoly poly, unsigned int *work,
                   int nitems) {
@@ -223,7 +232,7 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
 
         double nx = 0.0, ny = 0.0, nz = 0.0, ns = q;
         if (pbeg + lane < pend) {
-            const int i = pbeg + lane;
+            const int i = perm ? perm[pbeg + lane] : pbeg + lane;
             nx = px[i];
             ny = py[i];
             nz = pz[i];
@@ -233,7 +242,7 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
             const int cnt = min(kChunk, pend - pos);
             const double cx = nx, cy = ny, cz = nz, cs = ns;
             if (pos + kChunk + lane < pend) {   // prefetch the next chunk
-                const int i = pos + kChunk + lane;
+                const int i = perm ? perm[pos + kChunk + lane] : pos + kChunk + lane;
                 nx = px[i];
                 ny = py[i];
                 nz = pz[i];
@@ -456,7 +465,8 @@ __device__ __forceinline__ void plane_from_smem(double (&g)[8][2][3], int hh, do
 
 template <int W, bool PUSH>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, PIF_INTERP_MINB)
-interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ cell_start,
+interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
+                  const int32_t *__restrict__ cell_start,
                   const double4 *__restrict__ field, int seg, int nseg, double beta,
                   const EsPoly poly, PushParams pp, int32_t *__restrict__ key,
                   int32_t *__restrict__ rank, int32_t *__restrict__ count,
@@ -494,12 +504,14 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ cell_start,
         if (pbeg == pend) continue;
         const int64_t yrow = (iy + r) % n;
 
-        // prefetch the first chunk (positions, velocities) before the window
+        // prefetch the first chunk (positions, velocities, id) before the window
         double nx = 0.0, ny = 0.0, nz = 0.0, nvx = 0.0, nvy = 0.0, nvz = 0.0;
+        int64_t nid = 0;
         if (pbeg + lane < pend) {
-            const int i = pbeg + lane;
+            const int i = perm ? perm[pbeg + lane] : pbeg + lane;
             nx = P.x[i]; ny = P.y[i]; nz = P.z[i];
             if (PUSH) { nvx = P.vx[i]; nvy = P.vy[i]; nvz = P.vz[i]; }
+            if (perm || !PUSH) nid = P.id[i];
         }
         // window: slot s = c4 + 4h holds plane z == s (mod 8) of [k0, k0+8)
         double g[8][2][3];
@@ -516,14 +528,16 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ cell_start,
         for (int pos = pbeg; pos < pend; pos += kChunk) {
             const int cnt = min(kChunk, pend - pos);
             const double x0 = nx, y0 = ny, z0 = nz, vx0 = nvx, vy0 = nvy, vz0 = nvz;
+            const int64_t id0 = nid;
             if (PUSH && rank_idx >= 0) {
                 rank[rank_idx] = rank_val;
                 rank_idx = -1;
             }
             if (pos + kChunk + lane < pend) {   // prefetch the next chunk
-                const int i = pos + kChunk + lane;
+                const int i = perm ? perm[pos + kChunk + lane] : pos + kChunk + lane;
                 nx = P.x[i]; ny = P.y[i]; nz = P.z[i];
                 if (PUSH) { nvx = P.vx[i]; nvy = P.vy[i]; nvz = P.vz[i]; }
+                if (perm || !PUSH) nid = P.id[i];
             }
             chunk_weights<W, true>(st, tab, poly, lane, cnt, x0, y0, z0, 1.0, false, h, beta);
             int j = 0;
@@ -554,14 +568,15 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ cell_start,
                     double x = x0, y = y0, z = z0;
                     double vx = vx0, vy = vy0, vz = vz0;
                     boris_one(pp, E0, E1, E2, x, y, z, vx, vy, vz, dg);
-                    P.x[i] = x; P.y[i] = y; P.z[i] = z;
-                    P.vx[i] = vx; P.vy[i] = vy; P.vz[i] = vz;
+                    Q.x[i] = x; Q.y[i] = y; Q.z[i] = z;
+                    Q.vx[i] = vx; Q.vy[i] = vy; Q.vz[i] = vz;
+                    if (perm) Q.id[i] = id0;
                     const int kk = cell_key(x, y, z, h, pp.w, n);
                     key[i] = kk;
                     rank_val = atomicAdd(&count[kk], 1);
                     rank_idx = i;
                 } else {
-                    const int64_t o = 3 * P.id[i];
+                    const int64_t o = 3 * id0;
                     E_out[o] = E0;
                     E_out[o + 1] = E1;
                     E_out[o + 2] = E2;
@@ -613,7 +628,8 @@ __global__ void spread_generic_kernel(pif_soa_t P, const double *__restrict__ st
     }
 }
 
-__global__ void interp_generic_kernel(pif_soa_t P, const double4 *__restrict__ field, double beta,
+__global__ void interp_generic_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
+                                      const double4 *__restrict__ field, double beta,
                                       PushParams pp, int push, int32_t *__restrict__ key,
                                       int32_t *__restrict__ rank, int32_t *__restrict__ count,
                                       double *__restrict__ partials, double *__restrict__ E_out) {
@@ -623,9 +639,10 @@ __global__ void interp_generic_kernel(pif_soa_t P, const double4 *__restrict__ f
     double dg[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P.count;
          i += (int64_t)gridDim.x * blockDim.x) {
-        axis_stencil(P.x[i], pp.h, w, beta, n, wx, ixs);
-        axis_stencil(P.y[i], pp.h, w, beta, n, wy, iys);
-        axis_stencil(P.z[i], pp.h, w, beta, n, wz, izs);
+        const int64_t src = perm ? perm[i] : i;   // read in cell order, write at i
+        axis_stencil(P.x[src], pp.h, w, beta, n, wx, ixs);
+        axis_stencil(P.y[src], pp.h, w, beta, n, wy, iys);
+        axis_stencil(P.z[src], pp.h, w, beta, n, wz, izs);
         double l0[kMaxW], l1[kMaxW], l2[kMaxW];
         for (int c = 0; c < w; ++c) l0[c] = l1[c] = l2[c] = 0.0;
         for (int a = 0; a < w; ++a)
@@ -646,16 +663,18 @@ __global__ void interp_generic_kernel(pif_soa_t P, const double4 *__restrict__ f
             e2 = __dadd_rn(e2, __dmul_rn(l2[c], wz[c]));
         }
         if (push) {
-            double x = P.x[i], y = P.y[i], z = P.z[i];
-            double vx = P.vx[i], vy = P.vy[i], vz = P.vz[i];
+            double x = P.x[src], y = P.y[src], z = P.z[src];
+            double vx = P.vx[src], vy = P.vy[src], vz = P.vz[src];
+            const int64_t id = P.id[src];
             boris_one(pp, e0, e1, e2, x, y, z, vx, vy, vz, dg);
-            P.x[i] = x; P.y[i] = y; P.z[i] = z;
-            P.vx[i] = vx; P.vy[i] = vy; P.vz[i] = vz;
+            Q.x[i] = x; Q.y[i] = y; Q.z[i] = z;
+            Q.vx[i] = vx; Q.vy[i] = vy; Q.vz[i] = vz;
+            Q.id[i] = id;
             const int kk = cell_key(x, y, z, pp.h, w, n);
             key[i] = kk;
             rank[i] = atomicAdd(&count[kk], 1);
         } else {
-            const int64_t o = 3 * P.id[i];
+            const int64_t o = 3 * P.id[src];
             E_out[o] = e0;
             E_out[o + 1] = e1;
             E_out[o + 2] = e2;
@@ -828,8 +847,24 @@ static EsPoly device_poly(const Plan &p) {
     return e;
 }
 
-int launch_spread(Plan &p, const pif_soa_t &P, const double *strengths, double q,
-                  cudaStream_t s) {
+int launch_bin_perm(Plan &p, const int32_t *key, const int32_t *rank, int64_t M, int32_t *perm,
+                    cudaStream_t s) {
+    size_t tmp = p.scan_tmp_bytes;
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(p.scan_tmp, tmp, p.cell_count, p.cell_start,
+                                                  (int)(p.n3 + 1), s);
+    if (e != cudaSuccess) return fail_cuda(e, "cell scan");
+    if (M > 0) {
+        bin_perm_kernel<<<grid_for(M, 256, p.sm_count), 256, 0, s>>>(key, rank, p.cell_start, M,
+                                                                      perm);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return fail_cuda(e, "bin_perm_kernel");
+    }
+    return fail_cuda(cudaMemsetAsync(p.cell_count, 0, sizeof(int32_t) * (p.n3 + 1), s),
+                     "reset cell counts");
+}
+
+int launch_spread(Plan &p, const pif_soa_t &P, const int32_t *perm, const double *strengths,
+                  double q, cudaStream_t s) {
     const EsPoly poly = device_poly(p);
     cudaError_t e = cudaMemsetAsync(p.grid, 0, sizeof(double) * p.n3, s);
     if (e != cudaSuccess) return fail_cuda(e, "zero grid");
@@ -844,7 +879,8 @@ int launch_spread(Plan &p, const pif_soa_t &P, const double *strengths, double q
     case W: {                                                                                \
         auto k = spread_mma_kernel<W>;                                                      \
         int blocks = persistent_blocks(k, threads, 0, p.sm_count);                           \
-        k<<<blocks, threads, 0, s>>>(P.x, P.y, P.z, P.id, strengths, q, p.cell_start, p.grid, \
+        k<<<blocks, threads, 0, s>>>(P.x, P.y, P.z, P.id, perm, strengths, q, p.cell_start,   \
+                                     p.grid,                                                 \
                                      p.n, p.seg, nseg, p.h, p.beta, poly, p.work, nitems);   \
         break;                                                                               \
     }
@@ -868,9 +904,10 @@ int launch_spread(Plan &p, const pif_soa_t &P, const double *strengths, double q
     return fail_cuda(cudaGetLastError(), "spread kernel");
 }
 
-int launch_interp(Plan &p, pif_soa_t &P, bool push, double half, double dt, const double *tq,
-                  const double *sq, int has_b, int e_kind, int32_t *key, int32_t *rank,
-                  double *diag, double *E_out, cudaStream_t s) {
+int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q, bool push,
+                  double half, double dt, const double *tq, const double *sq, int has_b,
+                  int e_kind, int32_t *key, int32_t *rank, double *diag, double *E_out,
+                  cudaStream_t s) {
     if (!p.field_valid) {
         set_error("no field grid: solve the fields before gathering");
         return PIF_ERR_STATE;
@@ -892,13 +929,15 @@ int launch_interp(Plan &p, pif_soa_t &P, bool push, double half, double dt, cons
             auto k = interp_mma_kernel<W, true>;                                             \
             blocks = persistent_blocks(k, threads, 0, p.sm_count);                            \
             if (blocks > p.partial_blocks) blocks = p.partial_blocks;                         \
-            k<<<blocks, threads, 0, s>>>(P, p.cell_start, field, p.seg, nseg, p.beta, poly, pp, \
+            k<<<blocks, threads, 0, s>>>(P, perm, Q, p.cell_start, field, p.seg, nseg, p.beta,   \
+                                         poly, pp,                                            \
                                          key, rank, p.cell_count, p.partials, E_out, p.work,   \
                                          nitems);                                             \
         } else {                                                                              \
             auto k = interp_mma_kernel<W, false>;                                            \
             blocks = persistent_blocks(k, threads, 0, p.sm_count);                            \
-            k<<<blocks, threads, 0, s>>>(P, p.cell_start, field, p.seg, nseg, p.beta, poly, pp, \
+            k<<<blocks, threads, 0, s>>>(P, perm, Q, p.cell_start, field, p.seg, nseg, p.beta,   \
+                                         poly, pp,                                            \
                                          key, rank, p.cell_count, p.partials, E_out, p.work,   \
                                          nitems);                                             \
         }                                                                                     \
@@ -920,7 +959,8 @@ int launch_interp(Plan &p, pif_soa_t &P, bool push, double half, double dt, cons
     } else {
         blocks = grid_for(P.count, 128, p.sm_count);
         if (blocks > p.partial_blocks) blocks = p.partial_blocks;
-        interp_generic_kernel<<<blocks, 128, 0, s>>>(P, field, p.beta, pp, push ? 1 : 0, key,
+        interp_generic_kernel<<<blocks, 128, 0, s>>>(P, perm, Q, field, p.beta, pp, push ? 1 : 0,
+                                                     key,
                                                      rank, p.cell_count, p.partials, E_out);
     }
     e = cudaGetLastError();

@@ -67,11 +67,14 @@ int launch_wrap(Plan &p, double *x, double *y, double *z, int64_t M, cudaStream_
 int launch_bin_keys(Plan &p, const pif_soa_t &src, int32_t *key, int32_t *rank, cudaStream_t s);
 int launch_bin_scatter(Plan &p, const pif_soa_t &src, pif_soa_t &dst, const int32_t *key,
                        const int32_t *rank, bool vel, cudaStream_t s);
-int launch_spread(Plan &p, const pif_soa_t &sorted, const double *strengths, double q,
+int launch_bin_perm(Plan &p, const int32_t *key, const int32_t *rank, int64_t M, int32_t *perm,
+                    cudaStream_t s);
+int launch_spread(Plan &p, const pif_soa_t &parts, const int32_t *perm, const double *strengths,
+                  double q, cudaStream_t s);
+int launch_interp(Plan &p, const pif_soa_t &src, const int32_t *perm, pif_soa_t &dst, bool push,
+                  double half, double dt, const double *tq, const double *sq, int has_b,
+                  int e_kind, int32_t *key, int32_t *rank, double *diag, double *E_out,
                   cudaStream_t s);
-int launch_interp(Plan &p, pif_soa_t &sorted, bool push, double half, double dt,
-                  const double *tq, const double *sq, int has_b, int e_kind, int32_t *key,
-                  int32_t *rank, double *diag, double *E_out, cudaStream_t s);
 int launch_particle_diag(Plan &p, const pif_soa_t &ps, int e_kind, double *diag, cudaStream_t s);
 int launch_modes_from_spec(Plan &p, double *modes, cudaStream_t s);
 int launch_solve_fields(Plan &p, const double *raw, int shape, double *rho_out, double *scalars,

@@ -110,14 +110,14 @@ class PifEngine:
             _native.call("pif_wrap_points", self.handle, cur.x, cur.y, cur.z, self.count, s)
             _native.call("pif_bin_keys", self.handle, ctypes.byref(cur),
                          self.parts.key.data_ptr(), self.parts.rank.data_ptr(), s)
-            self._scatter()
+            self._bin()
 
-    def _scatter(self):
-        src, dst = self._soa("cur"), self._soa("alt")
-        _native.call("pif_bin_scatter", self.handle, ctypes.byref(src), ctypes.byref(dst),
-                     self.parts.key.data_ptr(), self.parts.rank.data_ptr(), 1, self._stream())
-        self.parts.swap()
-        self.launches += 3      # CUB scan (2 kernels) + scatter
+    def _bin(self):
+        """Cell-ordered view: perm from the keys/ranks of the current buffer."""
+        _native.call("pif_bin_perm", self.handle, self.parts.key.data_ptr(),
+                     self.parts.rank.data_ptr(), self.count, self.parts.perm.data_ptr(),
+                     self._stream())
+        self.launches += 3      # CUB scan (2 kernels) + perm
 
     # -- stages -----------------------------------------------------------------
     def particle_diag(self):
@@ -127,10 +127,10 @@ class PifEngine:
         self.launches += 2
 
     def spread(self):
-        """Binned register-tiled spreading into the plan's fine grid."""
+        """Binned DMMA spreading into the plan's fine grid (reads through perm)."""
         cur = self._soa()
-        _native.call("pif_spread_sorted", self.handle, ctypes.byref(cur), None, self.q,
-                     self._stream())
+        _native.call("pif_spread_perm", self.handle, ctypes.byref(cur),
+                     self.parts.perm.data_ptr(), None, self.q, self._stream())
         self.launches += 1
 
     def modes(self):
@@ -154,17 +154,20 @@ class PifEngine:
         self.launches += 5      # poisson, energy, guard (2), pad; cuFFT Z2D not counted
 
     def interp_push(self):
-        """Fused gather + Boris push + next cell keys + diagnostic sums."""
-        cur = self._soa()
-        _native.call("pif_interp_push", self.handle, ctypes.byref(cur), self.half, self.dt,
+        """Fused gather + Boris push + next cell keys + diagnostic sums: reads the
+        current buffer in cell order (perm), writes the other one, swaps."""
+        src, dst = self._soa("cur"), self._soa("alt")
+        _native.call("pif_interp_push_perm", self.handle, ctypes.byref(src),
+                     self.parts.perm.data_ptr(), ctypes.byref(dst), self.half, self.dt,
                      self._tq, self._sq, self.has_b, self.e_kind, self.parts.key.data_ptr(),
                      self.parts.rank.data_ptr(), self.diag.data_ptr(), self._stream())
+        self.parts.swap()
         self.launches += 2
 
     def rebin(self):
-        """Scan the cell counts emitted by interp_push and scatter into cell order."""
+        """Scan the cell counts emitted by interp_push and rebuild perm."""
         if self.count:
-            self._scatter()
+            self._bin()
 
     def gather_push(self):
         self.interp_push()

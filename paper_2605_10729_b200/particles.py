@@ -103,9 +103,11 @@ def minimum_image(delta, L: float):
 class DeviceParticles:
     """Double-buffered SoA particle store in HBM (one per rank/GPU).
 
-    Buffer ``cur`` holds the particles in ES-stencil cell order after binning;
-    the interp+push kernel updates it in place and emits the next cell keys,
-    and binning scatters it into the other buffer, which becomes ``cur``.
+    Buffer ``cur`` holds the particles; ``perm`` lists them in ES-stencil cell
+    order (binning never moves particle data).  The gather+push kernel reads
+    ``cur`` through ``perm`` and writes the updated particles, in that order,
+    to the other buffer, which becomes ``cur``; it also emits their next cell
+    keys, from which binning rebuilds ``perm``.
     """
 
     FIELDS = ("x", "y", "z", "vx", "vy", "vz")
@@ -121,6 +123,7 @@ class DeviceParticles:
                     torch.empty(cap, dtype=torch.int64, device=self.device)]
         self.key = torch.empty(cap, dtype=torch.int32, device=self.device)
         self.rank = torch.empty(cap, dtype=torch.int32, device=self.device)
+        self.perm = torch.empty(cap, dtype=torch.int32, device=self.device)
         self.cur = 0
 
     @property

@@ -385,7 +385,9 @@ def big(cuda):
 def test_binning_sorts_by_stencil_cell(big):
     torch = big["torch"]
     eng, plan = big["eng"], big["plan"]
-    soa = eng.parts.soa[:, :eng.count]
+    perm = eng.parts.perm[:eng.count].long()
+    assert torch.equal(torch.sort(perm)[0], torch.arange(eng.count, device="cuda"))
+    soa = eng.parts.soa[:, :eng.count][:, perm]
     n, w, h = plan.n_up, plan.window.w, plan.h
     keys = []
     for d in range(3):
@@ -445,7 +447,7 @@ def test_gather_self_force_at_scale(big):
     from paper_2605_10729_b200 import _native
     import ctypes
     cur = eng._soa()
-    _native.call("pif_interp_sorted", eng.handle, ctypes.byref(cur), E.data_ptr(),
-                 _native.stream_handle())
+    _native.call("pif_interp_perm", eng.handle, ctypes.byref(cur), eng.parts.perm.data_ptr(),
+                 E.data_ptr(), _native.stream_handle())
     net = E.sum(dim=0).abs().max().item()
     assert net <= 1e-10 * E.abs().max().item() * M
