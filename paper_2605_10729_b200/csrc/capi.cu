@@ -206,6 +206,9 @@ int pif_plan_create(const pif_plan_desc_t *d, int device, pif_plan_t *out) {
     TRY(pif::dalloc(p, &p.cell_count, p.n3 + 1));
     TRY(pif::dalloc(p, &p.cell_start, p.n3 + 1));
     TRY(pif::dalloc(p, &p.work, 4));
+    p.n_segs = p.n * p.n * ((p.n + p.seg - 1) / p.seg);
+    TRY(pif::dalloc(p, &p.seg_parts, p.n_segs + 1));
+    TRY(pif::dalloc(p, &p.seg_off, p.n_segs + 1));
     TRY(pif::dalloc(p, &p.partials, (size_t)p.partial_blocks * pif::kDiagSlots));
     TRY(pif::dalloc(p, &p.maxbits, 8));
     {
@@ -221,6 +224,7 @@ int pif_plan_create(const pif_plan_desc_t *d, int device, pif_plan_t *out) {
             e = cudaMemcpy(p.shape_tab + p.N, d->shape_cic, sizeof(double) * p.N,
                            cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMemset(p.cell_count, 0, sizeof(int32_t) * (p.n3 + 1));
+        if (e == cudaSuccess) e = cudaMemset(p.seg_off, 0, sizeof(int) * (p.n_segs + 1));
         if (e == cudaSuccess) e = cudaMemset(p.field, 0, sizeof(double) * 4 * p.n3);
         if (e != cudaSuccess) {
             rc = pif::fail_cuda(e, "plan tables");

@@ -89,6 +89,31 @@ __global__ void bin_perm_kernel(const int32_t *__restrict__ key, const int32_t *
         perm[start[key[j]] + rank[j]] = (int32_t)j;
 }
 
+// work items: parts of <= kItemParticles particles of each non-empty z-segment
+__global__ void seg_parts_kernel(const int32_t *__restrict__ cell_start, int n, int seg, int nseg,
+                                 int nsegs, int *__restrict__ parts) {
+    for (int sidx = blockIdx.x * blockDim.x + threadIdx.x; sidx <= nsegs;
+         sidx += gridDim.x * blockDim.x) {
+        if (sidx == nsegs) {
+            parts[sidx] = 0;
+            continue;
+        }
+        const int col = sidx / nseg, sg = sidx - col * nseg;
+        const int base = col * n, k0 = sg * seg, k1 = min(k0 + seg, n);
+        const int c = cell_start[base + k1] - cell_start[base + k0];
+        parts[sidx] = (c + kItemParticles - 1) / kItemParticles;
+    }
+}
+
+__global__ void seg_items_kernel(const int *__restrict__ parts, const int *__restrict__ off,
+                                 int nsegs, int2 *__restrict__ items) {
+    for (int sidx = blockIdx.x * blockDim.x + threadIdx.x; sidx < nsegs;
+         sidx += gridDim.x * blockDim.x) {
+        const int o = off[sidx];
+        for (int j = 0; j < parts[sidx]; ++j) items[o + j] = make_int2(sidx, j);
+    }
+}
+
 // ----------------------------------------------------------------------------
 // DMMA building blocks
 // ----------------------------------------------------------------------------
@@ -201,7 +226,8 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
                   const int32_t *__restrict__ perm, const double *__restrict__ strengths, double q,
                   const int32_t *__restrict__ cell_start, double *__restrict__ grid, int n,
                   int seg, int nseg, double h, double beta, const EsPoly poly, unsigned int *work,
-                  int nitems) {
+                  const int2 *__restrict__ items, const int *__restrict__ n_items) {
+    const int nitems = *n_items;
     __shared__ WarpChunk stage[kWarpsPerBlock];
     __shared__ double tab[32];
     if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
@@ -216,12 +242,13 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
         if (lane == 0) item = (int)atomicAdd(work, 1u);
         item = __shfl_sync(kFull, item, 0);
         if (item >= nitems) break;
-        const int col = item / nseg, sg = item - col * nseg;
+        const int2 it = items[item];
+        const int col = it.x / nseg, sg = it.x - col * nseg;
         const int ix = col / n, iy = col - ix * n;
         const int k0 = sg * seg, k1 = min(k0 + seg, n);
         const int base = col * n;
-        const int pbeg = cell_start[base + k0], pend = cell_start[base + k1];
-        if (pbeg == pend) continue;
+        const int pbeg = cell_start[base + k0] + it.y * kItemParticles;
+        const int pend = min(pbeg + kItemParticles, cell_start[base + k1]);
         const int64_t yrow = (iy + r) % n;   // this lane's footprint row b = r
 
         double acc[8][2];
@@ -229,6 +256,7 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
         for (int a = 0; a < 8; ++a) acc[a][0] = acc[a][1] = 0.0;
         int k = k0;
         int cell_end = cell_start[base + k0 + 1];
+        while (cell_end <= pbeg) cell_end = cell_start[base + (++k) + 1];   // first cell
 
         double nx = 0.0, ny = 0.0, nz = 0.0, ns = q;
         if (pbeg + lane < pend) {
@@ -471,7 +499,8 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                   const EsPoly poly, PushParams pp, int32_t *__restrict__ key,
                   int32_t *__restrict__ rank, int32_t *__restrict__ count,
                   double *__restrict__ partials, double *__restrict__ E_out, unsigned int *work,
-                  int nitems) {
+                  const int2 *__restrict__ items, const int *__restrict__ n_items) {
+    const int nitems = *n_items;
     __shared__ WarpChunk stage[kWarpsPerBlock];
     __shared__ double4 planes[kWarpsPerBlock][8][8];
     __shared__ double tab[32];
@@ -495,13 +524,16 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
         if (lane == 0) item = (int)atomicAdd(work, 1u);
         item = __shfl_sync(kFull, item, 0);
         if (item >= nitems) break;
-        const int col = item / nseg, sg = item - col * nseg;
+        const int2 it = items[item];
+        const int col = it.x / nseg, sg = it.x - col * nseg;
         const int ix = col / n, iy = col - ix * n;
         const int k0 = sg * seg, k1 = min(k0 + seg, n);
         const int base = col * n;
         const int cb = cell_start[base + k0 + min(lane, k1 - k0)];   // seg <= 31
-        const int pbeg = __shfl_sync(kFull, cb, 0), pend = __shfl_sync(kFull, cb, k1 - k0);
-        if (pbeg == pend) continue;
+        const int pbeg = __shfl_sync(kFull, cb, 0) + it.y * kItemParticles;
+        const int pend = min(pbeg + kItemParticles, __shfl_sync(kFull, cb, k1 - k0));
+        int kf = k0;   // cell holding the item's first particle
+        while (__shfl_sync(kFull, cb, kf - k0 + 1) <= pbeg) ++kf;
         const int64_t yrow = (iy + r) % n;
 
         // prefetch the first chunk (positions, velocities, id) before the window
@@ -513,17 +545,17 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
             if (PUSH) { nvx = P.vx[i]; nvy = P.vy[i]; nvz = P.vz[i]; }
             if (perm || !PUSH) nid = P.id[i];
         }
-        // window: slot s = c4 + 4h holds plane z == s (mod 8) of [k0, k0+8)
+        // window: slot s = c4 + 4h holds plane z == s (mod 8) of [kf, kf+8)
         double g[8][2][3];
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
             const int s = c4 + 4 * hh;
-            load_plane(g, hh, field, ix, yrow, n, (k0 + ((s - k0) & 7)) % n);
+            load_plane(g, hh, field, ix, yrow, n, (kf + ((s - kf) & 7)) % n);
         }
-        int k = k0;
-        int cell_end = __shfl_sync(kFull, cb, 1);
+        int k = kf;
+        int cell_end = __shfl_sync(kFull, cb, kf - k0 + 1);
         prefetch_wait();   // previous item's outstanding prefetch
-        prefetch_plane(pf, field, ix, iy, n, (k0 + 8) % n, lane);
+        prefetch_plane(pf, field, ix, iy, n, (kf + 8) % n, lane);
 
         for (int pos = pbeg; pos < pend; pos += kChunk) {
             const int cnt = min(kChunk, pend - pos);
@@ -835,6 +867,8 @@ int launch_bin_scatter(Plan &p, const pif_soa_t &src, pif_soa_t &dst, const int3
         if (e != cudaSuccess) return fail_cuda(e, "bin_scatter_kernel");
     }
     dst.count = src.count;
+    const int rc = build_items(p, src.count, s);
+    if (rc != PIF_OK) return rc;
     return fail_cuda(cudaMemsetAsync(p.cell_count, 0, sizeof(int32_t) * (p.n3 + 1), s),
                      "reset cell counts");
 }
@@ -845,6 +879,27 @@ static EsPoly device_poly(const Plan &p) {
     EsPoly e;
     std::memcpy(&e, &p.poly, sizeof(e));
     return e;
+}
+
+int build_items(Plan &p, int64_t M, cudaStream_t s) {
+    const int64_t need = p.n_segs + M / kItemParticles + 1;
+    if (need > p.items_cap) {
+        if (p.items) cudaFree(p.items);
+        p.items = nullptr;
+        cudaError_t e = cudaMalloc(&p.items, sizeof(int2) * need);
+        if (e != cudaSuccess) return fail_cuda(e, "work item table");
+        p.items_cap = need;
+    }
+    const int nseg = (p.n + p.seg - 1) / p.seg;
+    seg_parts_kernel<<<grid_for(p.n_segs + 1, 256, p.sm_count), 256, 0, s>>>(
+        p.cell_start, p.n, p.seg, nseg, p.n_segs, p.seg_parts);
+    size_t tmp = p.scan_tmp_bytes;
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(p.scan_tmp, tmp, p.seg_parts, p.seg_off,
+                                                  p.n_segs + 1, s);
+    if (e != cudaSuccess) return fail_cuda(e, "segment scan");
+    seg_items_kernel<<<grid_for(p.n_segs, 256, p.sm_count), 256, 0, s>>>(p.seg_parts, p.seg_off,
+                                                                         p.n_segs, p.items);
+    return fail_cuda(cudaGetLastError(), "work item kernels");
 }
 
 int launch_bin_perm(Plan &p, const int32_t *key, const int32_t *rank, int64_t M, int32_t *perm,
@@ -859,6 +914,8 @@ int launch_bin_perm(Plan &p, const int32_t *key, const int32_t *rank, int64_t M,
         e = cudaGetLastError();
         if (e != cudaSuccess) return fail_cuda(e, "bin_perm_kernel");
     }
+    const int rc = build_items(p, M, s);
+    if (rc != PIF_OK) return rc;
     return fail_cuda(cudaMemsetAsync(p.cell_count, 0, sizeof(int32_t) * (p.n3 + 1), s),
                      "reset cell counts");
 }
@@ -871,7 +928,7 @@ int launch_spread(Plan &p, const pif_soa_t &P, const int32_t *perm, const double
     if (P.count == 0) return PIF_OK;
     if (p.w <= kMaxFastW) {
         const int nseg = (p.n + p.seg - 1) / p.seg;
-        const int nitems = p.n * p.n * nseg;
+        const int *nitems = p.seg_off + p.n_segs;
         e = cudaMemsetAsync(p.work, 0, sizeof(unsigned int), s);
         if (e != cudaSuccess) return fail_cuda(e, "zero work counter");
         const int threads = kWarpsPerBlock * 32;
@@ -881,7 +938,8 @@ int launch_spread(Plan &p, const pif_soa_t &P, const int32_t *perm, const double
         int blocks = persistent_blocks(k, threads, 0, p.sm_count);                           \
         k<<<blocks, threads, 0, s>>>(P.x, P.y, P.z, P.id, perm, strengths, q, p.cell_start,   \
                                      p.grid,                                                 \
-                                     p.n, p.seg, nseg, p.h, p.beta, poly, p.work, nitems);   \
+                                     p.n, p.seg, nseg, p.h, p.beta, poly, p.work, p.items,   \
+                                     nitems);                                                \
         break;                                                                               \
     }
         switch (p.w) {
@@ -919,7 +977,7 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
     int blocks = 1;
     if (P.count > 0 && p.w <= kMaxFastW) {
         const int nseg = (p.n + p.seg - 1) / p.seg;
-        const int nitems = p.n * p.n * nseg;
+        const int *nitems = p.seg_off + p.n_segs;
         e = cudaMemsetAsync(p.work, 0, sizeof(unsigned int), s);
         if (e != cudaSuccess) return fail_cuda(e, "zero work counter");
         const int threads = kWarpsPerBlock * 32;
@@ -932,14 +990,14 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
             k<<<blocks, threads, 0, s>>>(P, perm, Q, p.cell_start, field, p.seg, nseg, p.beta,   \
                                          poly, pp,                                            \
                                          key, rank, p.cell_count, p.partials, E_out, p.work,   \
-                                         nitems);                                             \
+                                         p.items, nitems);                                    \
         } else {                                                                              \
             auto k = interp_mma_kernel<W, false>;                                            \
             blocks = persistent_blocks(k, threads, 0, p.sm_count);                            \
             k<<<blocks, threads, 0, s>>>(P, perm, Q, p.cell_start, field, p.seg, nseg, p.beta,   \
                                          poly, pp,                                            \
                                          key, rank, p.cell_count, p.partials, E_out, p.work,   \
-                                         nitems);                                             \
+                                         p.items, nitems);                                    \
         }                                                                                     \
         break;                                                                                \
     }

@@ -18,6 +18,7 @@ constexpr int kMaxW = 17;          // eps >= 1e-16 (nufft.py:74)
 constexpr int kSub = 8;            // particles per warp sub-batch (fast kernels)
 constexpr int kWarpsPerBlock = 4;  // fast kernels: one work item per warp
 constexpr int kDiagSlots = 6;
+constexpr int kItemParticles = 1024;   // max particles per work item
 
 // polynomial coefficients for the interior window weights (es_fast.cuh)
 constexpr int kEsDegHost = 14;
@@ -45,6 +46,13 @@ struct Plan {
     void *scan_tmp = nullptr;
     size_t scan_tmp_bytes = 0;
     unsigned int *work = nullptr;  // work counters for persistent kernels (4)
+    // work items = (z-segment, part) with parts of <= kItemParticles particles,
+    // rebuilt after every binning (heavy Penning segments split across warps)
+    int2 *items = nullptr;
+    int64_t items_cap = 0;
+    int *seg_parts = nullptr;      // n_segs + 1
+    int *seg_off = nullptr;        // n_segs + 1; seg_off[n_segs] = number of items
+    int n_segs = 0;
     double *partials = nullptr;    // per-block diagnostic / reduction partials
     int partial_blocks = 0;
     unsigned long long *maxbits = nullptr;  // atomics for max reductions (8)
@@ -67,6 +75,7 @@ int launch_wrap(Plan &p, double *x, double *y, double *z, int64_t M, cudaStream_
 int launch_bin_keys(Plan &p, const pif_soa_t &src, int32_t *key, int32_t *rank, cudaStream_t s);
 int launch_bin_scatter(Plan &p, const pif_soa_t &src, pif_soa_t &dst, const int32_t *key,
                        const int32_t *rank, bool vel, cudaStream_t s);
+int build_items(Plan &p, int64_t M, cudaStream_t s);
 int launch_bin_perm(Plan &p, const int32_t *key, const int32_t *rank, int64_t M, int32_t *perm,
                     cudaStream_t s);
 int launch_spread(Plan &p, const pif_soa_t &parts, const int32_t *perm, const double *strengths,
