@@ -180,6 +180,10 @@ int pif_type2_complex(pif_plan_t plan, const double *modes, const double *pts, i
  * iterations of 8 independent FMAs; *flops_out = flops issued. */
 int pif_probe_fp64(double *scratch, int blocks, int threads, int iters, void *stream,
                    double *flops_out);
+/* Profiling builds only (-DPIF_PHASE_TIMING): per-phase SM cycles of the
+ * gather+push kernel summed over warps since the last call, out[0..4] =
+ * {weights, DMMA gather, push, chunks, particles}; PIF_ERR_STATE otherwise. */
+int pif_debug_phase_cycles(unsigned long long *out);
 
 #ifdef __cplusplus
 }

@@ -73,6 +73,7 @@ SIGNATURES = {
     "pif_type1_complex": ([_P, _P, _P, _I64, _P, _P], _I),
     "pif_type2_complex": ([_P, _P, _P, _I64, _P, _P], _I),
     "pif_probe_fp64": ([_P, _I, _I, _I, _P, _D3], _I),
+    "pif_debug_phase_cycles": ([_P], _I),
 }
 
 

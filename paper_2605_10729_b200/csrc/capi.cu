@@ -286,6 +286,11 @@ int pif_plan_destroy(pif_plan_t plan) {
 
 int64_t pif_plan_device_bytes(pif_plan_t plan) { return plan ? plan->p.bytes : 0; }
 
+int pif_debug_phase_cycles(unsigned long long *out) {
+    if (!out) return pif::bad("null out");
+    return pif::debug_phase_cycles(out);
+}
+
 int pif_es_poly_info(int w, double beta, double *max_err, int *exact_mask) {
     if (w < 2 || w > pif::kMaxFastW || !(beta > 0)) return pif::bad("w must be in [2, 8]");
     pif::EsPolyHost P;

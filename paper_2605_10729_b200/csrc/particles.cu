@@ -487,6 +487,15 @@ __device__ __forceinline__ void plane_from_smem(double (&g)[8][2][3], int hh, do
     }
 }
 
+#ifdef PIF_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[8];
+#define PHASE_MARK(v) long long v = clock64()
+#define PHASE_ADD(slot, a, b) ph[slot] += (unsigned long long)((b) - (a))
+#else
+#define PHASE_MARK(v)
+#define PHASE_ADD(slot, a, b)
+#endif
+
 #ifndef PIF_INTERP_MINB
 #define PIF_INTERP_MINB 2
 #endif
@@ -518,6 +527,9 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
     // atomic's round trip overlaps the next chunk's work
     int64_t rank_idx = -1;
     int rank_val = 0;
+#ifdef PIF_PHASE_TIMING
+    unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
 
     for (;;) {
         int item = 0;
@@ -571,7 +583,10 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                 if (PUSH) { nvx = P.vx[i]; nvy = P.vy[i]; nvz = P.vz[i]; }
                 if (perm || !PUSH) nid = P.id[i];
             }
+            PHASE_MARK(t0);
             chunk_weights<W, true>(st, tab, poly, lane, cnt, x0, y0, z0, 1.0, false, h, beta);
+            PHASE_MARK(t1);
+            PHASE_ADD(0, t0, t1);
             int j = 0;
             while (j < cnt) {
                 const int gp = pos + j;
@@ -593,6 +608,8 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                 j += m;
             }
             __syncwarp();
+            PHASE_MARK(t2);
+            PHASE_ADD(1, t1, t2);
             if (lane < cnt) {
                 const int64_t i = pos + lane;
                 const double E0 = st.E[0][lane], E1 = st.E[1][lane], E2 = st.E[2][lane];
@@ -615,8 +632,18 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                 }
             }
             __syncwarp();
+            PHASE_MARK(t3);
+            PHASE_ADD(2, t2, t3);
+#ifdef PIF_PHASE_TIMING
+            ph[3] += 1;
+            ph[4] += (unsigned long long)cnt;
+#endif
         }
     }
+#ifdef PIF_PHASE_TIMING
+    if (lane == 0)
+        for (int i = 0; i < 5; ++i) atomicAdd(&g_phase_cycles[i], ph[i]);
+#endif
     prefetch_wait();
     if (PUSH && rank_idx >= 0) rank[rank_idx] = rank_val;
     if (PUSH) block_diag_store(dg, partials);
@@ -900,6 +927,21 @@ int build_items(Plan &p, int64_t M, cudaStream_t s) {
     seg_items_kernel<<<grid_for(p.n_segs, 256, p.sm_count), 256, 0, s>>>(p.seg_parts, p.seg_off,
                                                                          p.n_segs, p.items);
     return fail_cuda(cudaGetLastError(), "work item kernels");
+}
+
+int debug_phase_cycles(unsigned long long *out) {
+#ifdef PIF_PHASE_TIMING
+    cudaError_t e = cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 8);
+    if (e == cudaSuccess) {
+        unsigned long long z[8] = {0};
+        e = cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+    }
+    return fail_cuda(e, "phase counters");
+#else
+    (void)out;
+    set_error("built without PIF_PHASE_TIMING");
+    return PIF_ERR_STATE;
+#endif
 }
 
 int launch_bin_perm(Plan &p, const int32_t *key, const int32_t *rank, int64_t M, int32_t *perm,
