@@ -68,6 +68,7 @@ __global__ void bin_scatter_kernel(pif_soa_t src, pif_soa_t dst, const int32_t *
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M;
          i += (int64_t)gridDim.x * blockDim.x) {
         int64_t d = (int64_t)start[key[i]] + rank[i];
+        PIF_CHECK(d >= 0 && d < M);
         dst.x[d] = src.x[i];
         dst.y[d] = src.y[i];
         dst.z[d] = src.z[i];
@@ -85,8 +86,10 @@ __global__ void bin_perm_kernel(const int32_t *__restrict__ key, const int32_t *
                                 const int32_t *__restrict__ start, int64_t M,
                                 int32_t *__restrict__ perm) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < M;
-         j += (int64_t)gridDim.x * blockDim.x)
+         j += (int64_t)gridDim.x * blockDim.x) {
+        PIF_CHECK(start[key[j]] + rank[j] >= 0 && start[key[j]] + rank[j] < M);
         perm[start[key[j]] + rank[j]] = (int32_t)j;
+    }
 }
 
 // work items: parts of <= kItemParticles particles of each non-empty z-segment
@@ -209,6 +212,7 @@ __device__ __forceinline__ void spread_flush_plane(double (&acc)[8][2], int k, i
 #pragma unroll
         for (int a = 0; a < W; ++a) {
             const double v = j ? acc[a][1] : acc[a][0];
+            PIF_CHECK(((int64_t)((ix + a) % n) * n + yrow) * n + z < (int64_t)n * n * n);
             if (v != 0.0) atomicAdd(grid + ((int64_t)((ix + a) % n) * n + yrow) * n + z, v);
         }
 #pragma unroll
@@ -289,6 +293,7 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
                 const int m = min(4, min(pos + cnt, cell_end) - gp);
                 const bool ok = c4 < m;
                 const int pj = ok ? j + c4 : j;
+                PIF_CHECK(m > 0 && pj < kChunk && k >= k0 && k < k1);
                 const double wyb = ok ? st.wy[pj][r] : 0.0;
                 const double bz = st.wz[pj][(r - k) & 7];
 #pragma unroll
@@ -400,6 +405,7 @@ __device__ __forceinline__ void load_plane(double (&g)[8][2][3], int hh, const d
     for (int a = 0; a < 8; ++a) {
         int xa = ix + a;
         xa = xa >= n ? xa - n : xa;
+        PIF_CHECK(xa >= 0 && xa < n && yrow >= 0 && yrow < n && z >= 0 && z < n);
         const double4 f = field[((int64_t)xa * n + yrow) * n + z];
         g[a][hh][0] = f.x;
         g[a][hh][1] = f.y;
@@ -604,6 +610,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                     continue;
                 }
                 const int m = min(8, min(pos + cnt, cell_end) - gp);
+                PIF_CHECK(m > 0 && j + m <= kChunk && k >= k0 && k < k1);
                 gather_sub(st, g, j, m, k, r, c4);
                 j += m;
             }
@@ -621,6 +628,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                     Q.vx[i] = vx; Q.vy[i] = vy; Q.vz[i] = vz;
                     if (perm) Q.id[i] = id0;
                     const int kk = cell_key(x, y, z, h, pp.w, n);
+                    PIF_CHECK(kk >= 0 && kk < n * n * n && i < P.count);
                     key[i] = kk;
                     rank_val = atomicAdd(&count[kk], 1);
                     rank_idx = i;

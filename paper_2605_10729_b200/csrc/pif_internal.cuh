@@ -9,6 +9,15 @@
 
 #include "../../include/pif_b200.h"
 
+// Bounds checks for debug builds (-DPIF_DEBUG_BOUNDS): compute-sanitizer is
+// not available on the GPU pool, so the kernels check their own indices.
+#ifdef PIF_DEBUG_BOUNDS
+#include <cassert>
+#define PIF_CHECK(cond) assert(cond)
+#else
+#define PIF_CHECK(cond) ((void)0)
+#endif
+
 namespace pif {
 
 // Fused-kernel specialisations exist for stencil widths up to this value; wider
