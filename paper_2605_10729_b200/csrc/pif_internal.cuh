@@ -69,6 +69,7 @@ struct Plan {
     cufftHandle d2z = 0, z2d3 = 0, z2z = 0;
     bool z2d_strided = false;      // Z2D writes the interleaved grid directly
     bool field_valid = false;
+    bool interp_ws = false;         // warp-specialised gather+push (env PIF_INTERP_WS=1: on)
     int sm_count = 148;
     int64_t bytes = 0;
     EsPolyHost poly{};              // interior weight polynomials for w <= 8
