@@ -359,39 +359,34 @@ def run_b200(a):
 
 
 def run_e2e(a, eng, torch, dist, world, per_gpu, glob, dev):
-    """pif_step-style use with host (pinned) particle arrays: per step H2D of
-    x, v, upload + wrap + bin, spread, D2Z, allreduce, fields, gather+push,
-    D2H of x, v, ids (cell order) and the field energy."""
+    """pif_step-style use with host (pinned) particle arrays in id order (the
+    reference's ParticleEnsemble layout): per step H2D of x, v (ids implied by
+    position), upload + wrap + bin, spread, D2Z, allreduce, fields,
+    gather+push, device scatter back to id order, D2H of x, v and the field
+    energy."""
     M = eng.count
+    lo = int(eng.parts.ids[eng.parts.cur][:M].min())
     xh = torch.empty((M, 3), dtype=torch.float64, pin_memory=True)
     vh = torch.empty((M, 3), dtype=torch.float64, pin_memory=True)
-    idh = torch.empty(M, dtype=torch.int64, pin_memory=True)
-    x, v, ids = eng.parts.download(sort_by_id=False)
-    xh.copy_(x)
-    vh.copy_(v)
-    idh.copy_(ids)
-    del x, v, ids
-    # the host arrays hold the state: D2H writes back into them, the next step
-    # uploads them again (pif_step on numpy arrays)
-    xo, vo, io = xh, vh, idh
     wo = torch.empty(1, dtype=torch.float64, pin_memory=True)
     xd = torch.empty((M, 3), dtype=torch.float64, device=dev)
     vd = torch.empty((M, 3), dtype=torch.float64, device=dev)
-    idd = torch.empty(M, dtype=torch.int64, device=dev)
+    idd = torch.arange(lo, lo + M, dtype=torch.int64, device=dev)
+    eng.to_id_order(xd, vd, lo)
+    xh.copy_(xd)
+    vh.copy_(vd)
 
     def one():
         xd.copy_(xh, non_blocking=True)
         vd.copy_(vh, non_blocking=True)
-        idd.copy_(idh, non_blocking=True)
         eng.load(xd, vd, idd)
         eng.deposit()
         eng.allreduce()
         eng.solve_fields()
         eng.gather_push()
-        soa = eng.parts.soa[:, :M]
-        xo.copy_(soa[0:3].t(), non_blocking=True)
-        vo.copy_(soa[3:6].t(), non_blocking=True)
-        io.copy_(eng.parts.ids[eng.parts.cur][:M], non_blocking=True)
+        eng.to_id_order(xd, vd, lo)
+        xh.copy_(xd, non_blocking=True)   # the host arrays hold the state
+        vh.copy_(vd, non_blocking=True)
         wo.copy_(eng.scalars[0:1], non_blocking=True)
 
     one()
@@ -410,10 +405,10 @@ def run_e2e(a, eng, torch, dist, world, per_gpu, glob, dev):
         tt = torch.tensor([T], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         T = float(tt[0])
-    return {"value": glob * K / T, "unit": UNIT, "h2d_bytes_per_step": M * (48 + 8) * world,
-            "d2h_bytes_per_step": (M * (48 + 8) + 8) * world, "steps": K,
-            "api": "PifEngine.load (host pinned x,v,ids) -> deposit -> allreduce -> "
-                   "solve_fields -> gather_push -> D2H x,v,ids + W"}
+    return {"value": glob * K / T, "unit": UNIT, "h2d_bytes_per_step": M * 48 * world,
+            "d2h_bytes_per_step": (M * 48 + 8) * world, "steps": K,
+            "api": "pif_step-style: host pinned x,v (id order) -> PifEngine.load -> deposit -> "
+                   "allreduce -> solve_fields -> gather_push -> id-order scatter -> D2H x,v,W"}
 
 
 def main():

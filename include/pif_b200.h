@@ -163,6 +163,11 @@ int pif_interp_sorted(pif_plan_t plan, const pif_soa_t *sorted, double *E_out, v
 /* Same, reading the particles through perm (pif_bin_perm). */
 int pif_interp_perm(pif_plan_t plan, const pif_soa_t *parts, const int32_t *perm, double *E_out,
                     void *stream);
+/* Particles back to id order (ParticleEnsemble layout, particles.py:10-62):
+ * x_out/v_out are (M,3) AoS, row id - id0 (ids of the set must be
+ * id0 .. id0+M-1); v_out may be NULL. */
+int pif_soa_to_aos(pif_plan_t plan, const pif_soa_t *parts, int64_t id0, double *x_out,
+                   double *v_out, void *stream);
 /* Diagnostic sums of a particle set (Recorder.record, strategies.py:96-106). */
 int pif_particle_diag(pif_plan_t plan, const pif_soa_t *p, int e_kind, double *diag,
                       void *stream);

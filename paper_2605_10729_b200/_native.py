@@ -70,6 +70,7 @@ SIGNATURES = {
     "pif_interp_sorted": ([_P, _SOA, _P, _P], _I),
     "pif_interp_perm": ([_P, _SOA, _P, _P, _P], _I),
     "pif_particle_diag": ([_P, _SOA, _I, _P, _P], _I),
+    "pif_soa_to_aos": ([_P, _SOA, _I64, _P, _P, _P], _I),
     "pif_type1_complex": ([_P, _P, _P, _I64, _P, _P], _I),
     "pif_type2_complex": ([_P, _P, _P, _I64, _P, _P], _I),
     "pif_probe_fp64": ([_P, _I, _I, _I, _P, _D3], _I),

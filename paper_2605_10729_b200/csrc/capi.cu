@@ -445,6 +445,14 @@ int pif_interp_perm(pif_plan_t plan, const pif_soa_t *parts, const int32_t *perm
                               nullptr, nullptr, nullptr, E_out, s);
 }
 
+int pif_soa_to_aos(pif_plan_t plan, const pif_soa_t *parts, int64_t id0, double *x_out,
+                   double *v_out, void *stream) {
+    PLAN_CHECK();
+    if (!pif::soa_ok(parts, v_out != nullptr) || (parts->count > 0 && !x_out))
+        return pif::bad("invalid particle view / output");
+    return pif::launch_soa_to_aos(p, *parts, id0, x_out, v_out, s);
+}
+
 int pif_particle_diag(pif_plan_t plan, const pif_soa_t *ps, int e_kind, double *diag,
                       void *stream) {
     PLAN_CHECK();

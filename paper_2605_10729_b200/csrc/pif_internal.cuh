@@ -87,6 +87,8 @@ int launch_bin_scatter(Plan &p, const pif_soa_t &src, pif_soa_t &dst, const int3
                        const int32_t *rank, bool vel, cudaStream_t s);
 int build_items(Plan &p, int64_t M, cudaStream_t s);
 int debug_phase_cycles(unsigned long long *out);
+int launch_soa_to_aos(Plan &p, const pif_soa_t &P, int64_t id0, double *ox, double *ov,
+                      cudaStream_t s);
 int launch_bin_perm(Plan &p, const int32_t *key, const int32_t *rank, int64_t M, int32_t *perm,
                     cudaStream_t s);
 int launch_spread(Plan &p, const pif_soa_t &parts, const int32_t *perm, const double *strengths,

@@ -216,9 +216,22 @@ class PifEngine:
         self.allreduce()
         self.solve_fields()
 
+    def to_id_order(self, x_out=None, v_out=None, id0: int = 0):
+        """(M,3) x, v in id order (ids id0 .. id0+M-1) via a device scatter."""
+        torch = require_cuda()
+        M = self.count
+        if x_out is None:
+            x_out = torch.empty((M, 3), dtype=torch.float64, device=self.device)
+        if v_out is None:
+            v_out = torch.empty((M, 3), dtype=torch.float64, device=self.device)
+        cur = self._soa()
+        _native.call("pif_soa_to_aos", self.handle, ctypes.byref(cur), int(id0), x_out.data_ptr(),
+                     v_out.data_ptr(), self._stream())
+        return x_out, v_out
+
     def store_into(self, ens):
         """Copy the particles back into an AoS ensemble, original order."""
-        x, v, _ = self.parts.download(sort_by_id=True)
+        x, v = self.to_id_order()
         if is_torch(ens.x):
             ens.x = x.to(ens.x.device)
             ens.v = v.to(ens.v.device)
