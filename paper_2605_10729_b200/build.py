@@ -17,7 +17,7 @@ HEADERS = ["pif_internal.cuh", os.path.join("..", "..", "include", "pif_b200.h")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared"]
-LIBS = ["-lcufft", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
+LIBS = ["-lcufft", "-Xlinker", "-rpath=/usr/local/cuda/lib64", "-Xlinker", "-z,defs"]
 
 
 def _stale() -> bool:

@@ -81,6 +81,24 @@ __global__ void bin_scatter_kernel(pif_soa_t src, pif_soa_t dst, const int32_t *
     }
 }
 
+// particles back to id order as AoS (M,3) x and v: out[(id - id0)] = particle
+__global__ void soa_to_aos_by_id_kernel(pif_soa_t P, int64_t id0, double *__restrict__ ox,
+                                        double *__restrict__ ov) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P.count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t o = 3 * (P.id[i] - id0);
+        PIF_CHECK(o >= 0 && o < 3 * P.count);
+        ox[o] = P.x[i];
+        ox[o + 1] = P.y[i];
+        ox[o + 2] = P.z[i];
+        if (ov) {
+            ov[o] = P.vx[i];
+            ov[o + 1] = P.vy[i];
+            ov[o + 2] = P.vz[i];
+        }
+    }
+}
+
 // perm[start[key[j]] + rank[j]] = j: the cell-ordered view of a particle set
 __global__ void bin_perm_kernel(const int32_t *__restrict__ key, const int32_t *__restrict__ rank,
                                 const int32_t *__restrict__ start, int64_t M,
@@ -1227,6 +1245,13 @@ int build_items(Plan &p, int64_t M, cudaStream_t s) {
     seg_items_kernel<<<grid_for(p.n_segs, 256, p.sm_count), 256, 0, s>>>(p.seg_parts, p.seg_off,
                                                                          p.n_segs, p.items);
     return fail_cuda(cudaGetLastError(), "work item kernels");
+}
+
+int launch_soa_to_aos(Plan &p, const pif_soa_t &P, int64_t id0, double *ox, double *ov,
+                      cudaStream_t s) {
+    if (P.count == 0) return PIF_OK;
+    soa_to_aos_by_id_kernel<<<grid_for(P.count, 256, p.sm_count), 256, 0, s>>>(P, id0, ox, ov);
+    return fail_cuda(cudaGetLastError(), "soa_to_aos_by_id_kernel");
 }
 
 int debug_phase_cycles(unsigned long long *out) {
