@@ -80,3 +80,10 @@ def test_interior_weight_polynomials_are_accurate():
         if w >= 6:                     # eps <= 1e-5: every interior weight is a polynomial
             assert mask.value == 0, (w, mask.value)
         assert err[0] <= 4e-15, (w, err[0])   # polynomials in use meet the bound
+
+
+def test_no_unresolved_symbols_of_our_own():
+    from paper_2605_10729_b200 import _native
+    out = subprocess.run(["nm", "-D", "--undefined-only", _native.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    assert "pif" not in out, out
