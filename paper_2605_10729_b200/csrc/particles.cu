@@ -1293,7 +1293,7 @@ int launch_spread(Plan &p, const pif_soa_t &P, const int32_t *perm, const double
     cudaError_t e = cudaMemsetAsync(p.grid, 0, sizeof(double) * p.n3, s);
     if (e != cudaSuccess) return fail_cuda(e, "zero grid");
     if (P.count == 0) return PIF_OK;
-    if (p.w <= kMaxFastW) {
+    if (p.w <= kMaxFastW && !p.force_generic) {
         const int nseg = (p.n + p.seg - 1) / p.seg;
         const int *nitems = p.seg_off + p.n_segs;
         e = cudaMemsetAsync(p.work, 0, sizeof(unsigned int), s);
@@ -1342,7 +1342,7 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
     const double4 *field = reinterpret_cast<const double4 *>(p.field);
     cudaError_t e;
     int blocks = 1;
-    if (P.count > 0 && p.w <= kMaxFastW) {
+    if (P.count > 0 && p.w <= kMaxFastW && !p.force_generic) {
         const int nseg = (p.n + p.seg - 1) / p.seg;
         const int *nitems = p.seg_off + p.n_segs;
         e = cudaMemsetAsync(p.work, 0, sizeof(unsigned int), s);

@@ -70,6 +70,7 @@ struct Plan {
     bool z2d_strided = false;      // Z2D writes the interleaved grid directly
     bool field_valid = false;
     bool interp_ws = false;         // warp-specialised gather+push (env PIF_INTERP_WS=1: on)
+    bool force_generic = false;     // env PIF_FORCE_GENERIC=1: one-thread-per-particle kernels
     int sm_count = 148;
     int64_t bytes = 0;
     EsPolyHost poly{};              // interior weight polynomials for w <= 8

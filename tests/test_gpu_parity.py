@@ -451,3 +451,24 @@ def test_gather_self_force_at_scale(big):
                  E.data_ptr(), _native.stream_handle())
     net = E.sum(dim=0).abs().max().item()
     assert net <= 1e-10 * E.abs().max().item() * M
+
+
+def test_full_size_step_matches_oracle():
+    """One PD step at the benchmark mode count (64^3 modes, n = 128, w = 8) with
+    2^20 particles: rho_hat, E-at-particles and the pushed state against the CPU
+    oracle (multi-threaded like the reference's PD ranks)."""
+    import os
+    o = oracle()
+    spec = pb.landau_spec(N=64, ppm=4, dt=0.003125, steps=1, seed=0)
+    ens = pb.sample_landau(spec, 0)
+    plan = pb.make_plan(64, spec.L, 1e-7)
+    op = o.make_plan(64, spec.L, 1e-7)
+    rho = pb.deposit_charge(ens, plan).coeffs
+    run = o.PDRun(op, ens.x, ens.v, ens.q_per_particle, ens.m_per_particle, L=spec.L, dt=spec.dt,
+                  ranks=max(1, min(16, os.cpu_count() or 1)))
+    assert rel_l2(rho, run.rho) <= CONTRACT
+    assert rel_l2(rho, run.rho) <= 1e-13
+    E = pb.gather_efield(*pb.poisson_efield(pb.FourierField(64, spec.L, rho)), ens, plan)
+    Eo = o.gather_efield(o.poisson_efield(run.rho, spec.L), ens.x, op)
+    assert rel_l2(E, Eo) <= CONTRACT
+    assert rel_l2(E, Eo) <= 1e-12
