@@ -180,25 +180,75 @@ class PifEngine:
         r[6:7].copy_(self.scalars[1:2])
 
     # -- whole runs -----------------------------------------------------------------
-    def run(self, steps: int, *, timers=None):
+    def run(self, steps: int, *, timers=None, graph: bool | None = None):
         """Prime solve + record(0), then `steps` x (gather/push, solve, record)
         (strategies.py:285-303).  Returns the device record table (steps+1, 8):
-        [W, sum v.v, sum vx, sum vy, sum vz, sum phi_ext, guard, 0]."""
+        [W, sum v.v, sum vx, sum vy, sum vz, sum phi_ext, guard, 0].
+
+        graph=True (default when no timers are requested and steps >= 8):
+        the steps are replayed from a CUDA graph of two steps (the particle
+        buffers alternate), removing per-launch host overhead; the record slot
+        advances through a device-side counter."""
         torch = require_cuda()
         self.rec = torch.zeros((steps + 1, 8), dtype=torch.float64, device=self.device)
         dt = self.dtimers
         dt.enabled = timers is not None
+        if graph is None:
+            graph = timers is None and steps >= 8 and self._graph_ok()
         self.particle_diag()
         self._solve(dt)
         self.record(0)
-        for i in range(steps):
+        i = 0
+        if graph:
+            # two eager steps warm every allocation / plan, then capture
+            for _ in range(2):
+                self.gather_push()
+                self._solve(dt)
+                self.record(i + 1)
+                i += 1
+            pairs = (steps - i) // 2
+            if pairs > 0:
+                g = self._capture_pair(i + 1)
+                for _ in range(pairs):
+                    g.replay()
+                i += 2 * pairs
+        for k in range(i, steps):
             with dt.section("Gather"):
                 self.gather_push()
             self._solve(dt)
-            self.record(i + 1)
+            self.record(k + 1)
         if timers is not None:
             dt.flush(timers)
         return self.rec
+
+    def _graph_ok(self) -> bool:
+        # NCCL collectives can be captured, the in-process thread transport cannot
+        from .comm import TorchDistTransport
+        return self.comm is None or isinstance(self.comm.transport, TorchDistTransport)
+
+    def _capture_pair(self, first_slot: int):
+        """CUDA graph of two full steps recording into rec[slot], rec[slot+1]
+        with slot held on the device (advanced by 2 inside the graph)."""
+        torch = require_cuda()
+        self._slot = torch.tensor([first_slot], dtype=torch.int64, device=self.device)
+        self._row = torch.zeros((1, 8), dtype=torch.float64, device=self.device)
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(g, stream=side):
+                for _ in range(2):
+                    self.gather_push()
+                    self.deposit()
+                    self.allreduce()
+                    self.solve_fields()
+                    self._row[0, 0:1].copy_(self.scalars[0:1])
+                    self._row[0, 1:6].copy_(self.diag[0:5])
+                    self._row[0, 6:7].copy_(self.scalars[1:2])
+                    self.rec.index_copy_(0, self._slot, self._row)
+                    self._slot += 1
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        return g
 
     def _solve(self, dt):
         with dt.section("Scatter"):

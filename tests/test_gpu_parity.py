@@ -472,3 +472,22 @@ def test_full_size_step_matches_oracle():
     Eo = o.gather_efield(o.poisson_efield(run.rho, spec.L), ens.x, op)
     assert rel_l2(E, Eo) <= CONTRACT
     assert rel_l2(E, Eo) <= 1e-12
+
+
+def test_cuda_graph_run_matches_eager(cuda):
+    torch = cuda
+    from paper_2605_10729_b200.engine import PifEngine
+    spec = pb.landau_spec(N=16, ppm=16, dt=0.05, steps=20, seed=0)
+    ens = pb.sample_landau(spec, 0)
+    plan = pb.make_plan(16, spec.L, 1e-7)
+    tabs = []
+    for graph in (False, True):
+        eng = PifEngine(plan, ens.count, "cuda", q=ens.q_per_particle, m=ens.m_per_particle,
+                        externals=spec.externals(), dt=spec.dt)
+        eng.load(ens.x, ens.v, ens.ids)
+        tabs.append(eng.run(21, graph=graph).cpu().numpy())
+    a, b = tabs
+    assert np.all(b[:, 0] > 0)
+    assert np.max(np.abs(a[:, :6] - b[:, :6]) / np.maximum(np.abs(a[:, :6]), 1e-300)) <= 1e-12
+    ref = CFG["landau_trace"]
+    assert np.max(np.abs(b[:21, 0] - ref[:, 2]) / ref[:, 2]) <= 1e-10
