@@ -57,3 +57,34 @@ def test_nccl_pd_two_processes_matches_reference(cuda):
     for rank, _, prims, n in out:
         assert prims == ["allreduce"]
         assert n == 21          # one collective per step (+ the priming solve)
+
+
+def test_cli_under_torchrun_two_gpus(cuda, tmp_path):
+    """`torchrun -m paper_2605_10729_b200.cli --strategy pd` — one process per GPU."""
+    torch = cuda
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    import subprocess
+    import sys
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    out = tmp_path / "run"
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           "-m", "paper_2605_10729_b200.cli", "--benchmark", "landau", "--strategy", "pd",
+           "--modes", "16", "--ppm", "16", "--dt", "0.05", "--steps", "20",
+           "--ranks-space", "2", "--out-dir", str(out), "--log-comm"]
+    proc = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert proc.returncode == 0, proc.stderr[-3000:]
+    assert "final_field_energy=" in proc.stdout
+    import csv
+    with open(out / "diagnostics.csv") as f:
+        rows = list(csv.DictReader(f))
+    ref = golden("config1.npz")["landau_pd2_trace"][1:, 2]
+    got = np.array([float(r["field_energy"]) for r in rows])
+    assert np.max(np.abs(got - ref) / np.abs(ref)) <= 1e-10
+    with open(out / "timers.csv") as f:
+        assert {r["rank"] for r in csv.DictReader(f)} == {"0", "1"}
