@@ -101,7 +101,8 @@ void build_es_poly(int w, double beta, EsPolyHost *P, double *max_err) {
         if (u < 0) u = 0;
         return expl(B * (sqrtl(u) - 1.0L));
     };
-    for (int a = 1; a + 1 < w && a <= 6; ++a) {
+    // rows a = 1 .. (w-1)/2; weight w-1-a is the mirror p_a(-u) (es_fast.cuh)
+    for (int a = 1; 2 * a <= w - 1 && a <= 6; ++a) {
         long double y[kEsDegHost + 1], cheb[kEsDegHost + 1];
         for (int k = 0; k <= D; ++k) {
             const long double un = cosl(pi * (k + 0.5L) / (D + 1));
@@ -128,14 +129,22 @@ void build_es_poly(int w, double beta, EsPolyHost *P, double *max_err) {
             }
         }
         for (int k = 0; k <= D; ++k) P->c[a - 1][k] = (double)mono[k];
+        // check exactly the device evaluation: E(u^2) +/- u O(u^2), both weights
+        const double *cf = P->c[a - 1];
         double err = 0.0;
         for (int i = 0; i <= 4000; ++i) {
             const double f = i / 4000.0 * (1.0 - 1e-12);
-            const double u = 2.0 * f - 1.0;
-            double p = P->c[a - 1][D];
-            for (int k = D - 1; k >= 0; --k) p = std::fma(p, u, P->c[a - 1][k]);
-            const double e = std::fabs(p - (double)phi(1.0L - (2.0L / w) * (a + (long double)f)));
-            if (e > err) err = e;
+            const double u = 2.0 * f - 1.0, v = u * u;
+            double e = cf[D], o = cf[D - 1];
+            for (int k = D / 2 - 1; k >= 0; --k) {
+                e = std::fma(e, v, cf[2 * k]);
+                if (k < (D - 1) / 2) o = std::fma(o, v, cf[2 * k + 1]);
+            }
+            const double pa = std::fma(u, o, e), pb = std::fma(-u, o, e);
+            const long double fl = (long double)f;
+            const double ea = std::fabs(pa - (double)phi(1.0L - (2.0L / w) * (a + fl)));
+            const double eb = std::fabs(pb - (double)phi(1.0L - (2.0L / w) * (w - 1 - a + fl)));
+            err = std::max(err, std::max(ea, eb));
         }
         if (err > 4e-15) {
             P->exact_mask |= 1 << (a - 1);

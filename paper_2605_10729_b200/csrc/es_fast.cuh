@@ -70,14 +70,19 @@ namespace pif {
 // x = c - w/2, i0 = ceil(x) and f = i0 - x in [0, 1) (both steps exact), weight a
 // is phi(1 - (2/w)(a + f)).  For 1 <= a <= w-2 this is analytic on f in [0, 1]
 // (the sqrt branch points of phi sit at a + f = 0 and a + f = w), so it is
-// evaluated as a degree-kEsDeg polynomial in u = 2f - 1 (Horner, coefficients
-// from Chebyshev interpolation in extended precision at plan creation,
-// build_es_poly in capi.cu; max error < 4e-15 absolute, checked there).  The
-// two edge weights keep the exact formula.
+// a degree-kEsDeg polynomial p_a in u = 2f - 1 (coefficients from Chebyshev
+// interpolation in extended precision at plan creation, build_es_poly in
+// capi.cu).  phi is even, so weight w-1-a is p_a(-u): each mirrored pair is
+// evaluated from one even part E(u^2) and one odd part O(u^2) as E +/- u O,
+// half the Horner steps of two separate chains.  The error of exactly this
+// evaluation is checked on the host (< 4e-15 absolute).  The two edge weights
+// keep the exact formula.
 constexpr int kEsDeg = 14;
+constexpr int kEsEven = kEsDeg / 2;          // E has coefficients c[0], c[2], .., c[14]
+constexpr int kEsOdd = (kEsDeg - 1) / 2;     // O has coefficients c[1], c[3], .., c[13]
 
 struct EsPoly {
-    double c[kMaxFastW - 2][kEsDeg + 1];   // [a - 1][power]
+    double c[kMaxFastW - 2][kEsDeg + 1];   // [a - 1][power], rows a <= (w-1)/2 used
     int exact_mask;                        // bit a-1 set: evaluate weight a exactly
 };
 
@@ -90,15 +95,22 @@ __device__ __forceinline__ void es_axis_weights(double c, double beta, const EsP
     if (W > 1) wt[W - 1] = es_weight_fast(c, i0 + (double)(W - 1), inv_half, beta, tab);
     const double f = i0 - __dsub_rn(c, 0.5 * W);
     const double u = fma(2.0, f, -1.0);
+    const double v = u * u;
 #pragma unroll
-    for (int a = 1; a + 1 < W; ++a) {
+    for (int a = 1; 2 * a <= W - 1; ++a) {
+        const int b = W - 1 - a;
         if (P.exact_mask & (1 << (a - 1))) {
             wt[a] = es_weight_fast(c, i0 + (double)a, inv_half, beta, tab);
+            if (b != a) wt[b] = es_weight_fast(c, i0 + (double)b, inv_half, beta, tab);
         } else {
-            double p = P.c[a - 1][kEsDeg];
+            double e = P.c[a - 1][2 * kEsEven], o = P.c[a - 1][2 * kEsOdd + 1];
 #pragma unroll
-            for (int k = kEsDeg - 1; k >= 0; --k) p = fma(p, u, P.c[a - 1][k]);
-            wt[a] = p;
+            for (int k = kEsEven - 1; k >= 0; --k) {
+                e = fma(e, v, P.c[a - 1][2 * k]);
+                if (k < kEsOdd) o = fma(o, v, P.c[a - 1][2 * k + 1]);
+            }
+            wt[a] = fma(u, o, e);
+            if (b != a) wt[b] = fma(-u, o, e);
         }
     }
 }
@@ -107,35 +119,45 @@ __device__ __forceinline__ void es_axis_weights(double c, double beta, const EsP
 
 namespace pif {
 
-// All three axes at once: the 3*(w-2) interior Horner chains advance together
-// (power-outer loop) so a warp has 18 independent FMAs in flight per step.
+// All three axes at once: the 3 x (pairs) even/odd Horner chains advance
+// together (power-outer loop) so a warp has many independent FMAs in flight.
 template <int W>
 __device__ __forceinline__ void es_xyz_weights(const double (&c)[3], double beta, const EsPoly &P,
                                                const double *tab, double (&wt)[3][W]) {
     constexpr double inv_half = 2.0 / W;
-    constexpr int NI = W > 2 ? W - 2 : 0;
-    double u[3], i0[3];
+    constexpr int NP = (W - 1) / 2;          // pairs (a, w-1-a), a = 1 .. NP (+ middle if odd)
+    double u[3], v[3], i0[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
         i0[d] = stencil_start(c[d], W);
         u[d] = fma(2.0, i0[d] - __dsub_rn(c[d], 0.5 * W), -1.0);
+        v[d] = u[d] * u[d];
     }
-    if (NI > 0) {
-        double p[3][NI > 0 ? NI : 1];
+    if (NP > 0) {
+        double e[3][NP > 0 ? NP : 1], o[3][NP > 0 ? NP : 1];
 #pragma unroll
         for (int d = 0; d < 3; ++d)
 #pragma unroll
-            for (int a = 0; a < NI; ++a) p[d][a] = P.c[a][kEsDeg];
+            for (int a = 0; a < NP; ++a) {
+                e[d][a] = P.c[a][2 * kEsEven];
+                o[d][a] = P.c[a][2 * kEsOdd + 1];
+            }
 #pragma unroll
-        for (int k = kEsDeg - 1; k >= 0; --k)
+        for (int k = kEsEven - 1; k >= 0; --k)
 #pragma unroll
             for (int d = 0; d < 3; ++d)
 #pragma unroll
-                for (int a = 0; a < NI; ++a) p[d][a] = fma(p[d][a], u[d], P.c[a][k]);
+                for (int a = 0; a < NP; ++a) {
+                    e[d][a] = fma(e[d][a], v[d], P.c[a][2 * k]);
+                    if (k < kEsOdd) o[d][a] = fma(o[d][a], v[d], P.c[a][2 * k + 1]);
+                }
 #pragma unroll
         for (int d = 0; d < 3; ++d)
 #pragma unroll
-            for (int a = 0; a < NI; ++a) wt[d][a + 1] = p[d][a];
+            for (int a = 0; a < NP; ++a) {
+                wt[d][a + 1] = fma(u[d], o[d][a], e[d][a]);
+                if (W - 2 - a != a + 1) wt[d][W - 2 - a] = fma(-u[d], o[d][a], e[d][a]);
+            }
     }
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
@@ -143,7 +165,7 @@ __device__ __forceinline__ void es_xyz_weights(const double (&c)[3], double beta
         if (W > 1) wt[d][W - 1] = es_weight_fast(c[d], i0[d] + (double)(W - 1), inv_half, beta, tab);
 #pragma unroll
         for (int a = 1; a + 1 < W; ++a)
-            if (P.exact_mask & (1 << (a - 1)))
+            if (P.exact_mask & (1 << (min(a, W - 1 - a) - 1)))
                 wt[d][a] = es_weight_fast(c[d], i0[d] + (double)a, inv_half, beta, tab);
     }
 }
