@@ -80,6 +80,9 @@ namespace pif {
 constexpr int kEsDeg = 14;
 constexpr int kEsEven = kEsDeg / 2;          // E has coefficients c[0], c[2], .., c[14]
 constexpr int kEsOdd = (kEsDeg - 1) / 2;     // O has coefficients c[1], c[3], .., c[13]
+// From this width on every interior weight is a polynomial (launchers route a
+// plan with exact_mask != 0 to the generic kernels), so no exact branch is compiled.
+constexpr int kPolyOnlyW = 6;
 
 struct EsPoly {
     double c[kMaxFastW - 2][kEsDeg + 1];   // [a - 1][power], rows a <= (w-1)/2 used
@@ -99,7 +102,7 @@ __device__ __forceinline__ void es_axis_weights(double c, double beta, const EsP
 #pragma unroll
     for (int a = 1; 2 * a <= W - 1; ++a) {
         const int b = W - 1 - a;
-        if (P.exact_mask & (1 << (a - 1))) {
+        if (W < kPolyOnlyW && (P.exact_mask & (1 << (a - 1)))) {
             wt[a] = es_weight_fast(c, i0 + (double)a, inv_half, beta, tab);
             if (b != a) wt[b] = es_weight_fast(c, i0 + (double)b, inv_half, beta, tab);
         } else {
@@ -165,7 +168,7 @@ __device__ __forceinline__ void es_xyz_weights(const double (&c)[3], double beta
         if (W > 1) wt[d][W - 1] = es_weight_fast(c[d], i0[d] + (double)(W - 1), inv_half, beta, tab);
 #pragma unroll
         for (int a = 1; a + 1 < W; ++a)
-            if (P.exact_mask & (1 << (min(a, W - 1 - a) - 1)))
+            if (W < kPolyOnlyW && (P.exact_mask & (1 << (min(a, W - 1 - a) - 1))))
                 wt[d][a] = es_weight_fast(c[d], i0[d] + (double)a, inv_half, beta, tab);
     }
 }

@@ -29,10 +29,11 @@ __device__ __forceinline__ int cell_index_of(double c, int w, int n) {
     return pmod((int)stencil_start(c, w), n);
 }
 
-__device__ __forceinline__ int cell_key(double x, double y, double z, double h, int w, int n) {
-    int kx = cell_index_of(axis_coord(x, h), w, n);
-    int ky = cell_index_of(axis_coord(y, h), w, n);
-    int kz = cell_index_of(axis_coord(z, h), w, n);
+__device__ __forceinline__ int cell_key(double x, double y, double z, double h, double rh, int w,
+                                        int n) {
+    int kx = cell_index_of(axis_coord(x, h, rh), w, n);
+    int ky = cell_index_of(axis_coord(y, h, rh), w, n);
+    int kz = cell_index_of(axis_coord(z, h, rh), w, n);
     return (kx * n + ky) * n + kz;
 }
 
@@ -53,9 +54,10 @@ __global__ void bin_keys_kernel(const double *__restrict__ x, const double *__re
                                 const double *__restrict__ z, int64_t M, double h, int w, int n,
                                 int32_t *__restrict__ key, int32_t *__restrict__ rank,
                                 int32_t *__restrict__ count) {
+    const double rh = __drcp_rn(h);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M;
          i += (int64_t)gridDim.x * blockDim.x) {
-        int k = cell_key(x[i], y[i], z[i], h, w, n);
+        int k = cell_key(x[i], y[i], z[i], h, rh, w, n);
         key[i] = k;
         rank[i] = atomicAdd(&count[k], 1);
     }
@@ -179,10 +181,11 @@ __device__ __forceinline__ void chunk_zero(WarpChunk &st, int lane) {
 template <int W, bool XYZ>
 __device__ __forceinline__ void chunk_weights(WarpChunk &st, const double *tab, const EsPoly &P,
                                               int lane, int cnt, double x, double y, double z,
-                                              double s, bool scale, double h, double beta) {
+                                              double s, bool scale, double h, double rh,
+                                              double beta) {
     if (lane < cnt) {
         if (XYZ) {
-            const double c[3] = {axis_coord(x, h), axis_coord(y, h), axis_coord(z, h)};
+            const double c[3] = {axis_coord(x, h, rh), axis_coord(y, h, rh), axis_coord(z, h, rh)};
             double wt[3][W];
             es_xyz_weights<W>(c, beta, P, tab, wt);
 #pragma unroll
@@ -193,13 +196,13 @@ __device__ __forceinline__ void chunk_weights(WarpChunk &st, const double *tab, 
             }
         } else {
             double wt[W];
-            es_axis_weights<W>(axis_coord(x, h), beta, P, tab, wt);
+            es_axis_weights<W>(axis_coord(x, h, rh), beta, P, tab, wt);
 #pragma unroll
             for (int a = 0; a < W; ++a) st.wx[a][lane] = scale ? __dmul_rn(s, wt[a]) : wt[a];
-            es_axis_weights<W>(axis_coord(y, h), beta, P, tab, wt);
+            es_axis_weights<W>(axis_coord(y, h, rh), beta, P, tab, wt);
 #pragma unroll
             for (int a = 0; a < W; ++a) st.wy[lane][a] = wt[a];
-            es_axis_weights<W>(axis_coord(z, h), beta, P, tab, wt);
+            es_axis_weights<W>(axis_coord(z, h, rh), beta, P, tab, wt);
 #pragma unroll
             for (int a = 0; a < W; ++a) st.wz[lane][a] = wt[a];
         }
@@ -250,6 +253,7 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
                   int seg, int nseg, double h, double beta, const EsPoly poly, unsigned int *work,
                   const int2 *__restrict__ items, const int *__restrict__ n_items) {
     const int nitems = *n_items;
+    const double rh = __drcp_rn(h);
     __shared__ WarpChunk stage[kWarpsPerBlock];
     __shared__ double tab[32];
     if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
@@ -298,7 +302,7 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
                 nz = pz[i];
                 if (strengths) ns = strengths[pid[i]];
             }
-            chunk_weights<W, false>(st, tab, poly, lane, cnt, cx, cy, cz, cs, true, h, beta);
+            chunk_weights<W, false>(st, tab, poly, lane, cnt, cx, cy, cz, cs, true, h, rh, beta);
             int j = 0;
             while (j < cnt) {
                 const int gp = pos + j;
@@ -349,7 +353,8 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
 // ----------------------------------------------------------------------------
 
 struct PushParams {
-    double half, dt, L, h;
+    double half, dt, L, h, rh;
+    double ext_c, ext_xy, ext_z, pot_xy, pot_z;   // L/2, -15/L, 30/L, 7.5/L, 15/L
     double tq[3], sq[3];
     int has_b, e_kind, n, w;
 };
@@ -363,10 +368,10 @@ __device__ __forceinline__ void boris_one(const PushParams &pp, double E0, doubl
     double et0 = E0, et1 = E1, et2 = E2;
     const double L = pp.L;
     if (pp.e_kind == PIF_EXT_QUADRUPOLE) {
-        const double c = L / 2.0;
-        et0 = __dadd_rn(et0, __dmul_rn(-15.0 / L, __dsub_rn(x, c)));
-        et1 = __dadd_rn(et1, __dmul_rn(-15.0 / L, __dsub_rn(y, c)));
-        et2 = __dadd_rn(et2, __dmul_rn(30.0 / L, __dsub_rn(z, c)));
+        const double c = pp.ext_c;
+        et0 = __dadd_rn(et0, __dmul_rn(pp.ext_xy, __dsub_rn(x, c)));
+        et1 = __dadd_rn(et1, __dmul_rn(pp.ext_xy, __dsub_rn(y, c)));
+        et2 = __dadd_rn(et2, __dmul_rn(pp.ext_z, __dsub_rn(z, c)));
     }
     const double hf = pp.half;
     double m0 = __dadd_rn(vx, __dmul_rn(hf, et0));
@@ -396,9 +401,9 @@ __device__ __forceinline__ void boris_one(const PushParams &pp, double E0, doubl
     dg[2] += vy;
     dg[3] += vz;
     if (pp.e_kind == PIF_EXT_QUADRUPOLE) {
-        const double c = L / 2.0;
+        const double c = pp.ext_c;
         const double dx = x - c, dy = y - c, dz = z - c;
-        dg[4] += (7.5 / L) * (dx * dx + dy * dy) - (15.0 / L) * (dz * dz);
+        dg[4] += pp.pot_xy * (dx * dx + dy * dy) - pp.pot_z * (dz * dz);
     }
 }
 
@@ -622,7 +627,7 @@ __device__ __forceinline__ void ws_particle_warp(PairShared &sh, const pif_soa_t
             Q.x[i] = q.x; Q.y[i] = q.y; Q.z[i] = q.z;
             Q.vx[i] = q.vx; Q.vy[i] = q.vy; Q.vz[i] = q.vz;
             if (perm) Q.id[i] = q.id;
-            const int kk = cell_key(q.x, q.y, q.z, h, pp.w, n);
+            const int kk = cell_key(q.x, q.y, q.z, h, pp.rh, pp.w, n);
             PIF_CHECK(kk >= 0 && kk < n * n * n);
             key[i] = kk;
             rank_val = atomicAdd(&count[kk], 1);
@@ -670,7 +675,7 @@ __device__ __forceinline__ void ws_particle_warp(PairShared &sh, const pif_soa_t
             }
             PHASE_MARK(t3);
             chunk_weights<W, true>(sh.stage[b], sh.tab, poly, lane, cnt, cur.x, cur.y, cur.z, 1.0,
-                                   false, h, beta);
+                                   false, h, pp.rh, beta);
             PHASE_MARK(t4);
             PHASE_ADD(0, t3, t4);
             if (b) {
@@ -900,7 +905,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                 if (perm || !PUSH) nid = P.id[i];
             }
             PHASE_MARK(t0);
-            chunk_weights<W, true>(st, tab, poly, lane, cnt, x0, y0, z0, 1.0, false, h, beta);
+            chunk_weights<W, true>(st, tab, poly, lane, cnt, x0, y0, z0, 1.0, false, h, pp.rh, beta);
             PHASE_MARK(t1);
             PHASE_ADD(0, t0, t1);
             int j = 0;
@@ -937,7 +942,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                     Q.x[i] = x; Q.y[i] = y; Q.z[i] = z;
                     Q.vx[i] = vx; Q.vy[i] = vy; Q.vz[i] = vz;
                     if (perm) Q.id[i] = id0;
-                    const int kk = cell_key(x, y, z, h, pp.w, n);
+                    const int kk = cell_key(x, y, z, h, pp.rh, pp.w, n);
                     PIF_CHECK(kk >= 0 && kk < n * n * n && i < P.count);
                     key[i] = kk;
                     rank_val = atomicAdd(&count[kk], 1);
@@ -973,7 +978,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
 
 __device__ __forceinline__ int axis_stencil(double xv, double h, int w, double beta, int n,
                                             double *wt, int *idx) {
-    const double c = axis_coord(xv, h);
+    const double c = axis_coord(xv, h, __drcp_rn(h));
     const double i0 = stencil_start(c, w);
     const double inv_half = 2.0 / w;
     for (int a = 0; a < w; ++a) {
@@ -1047,7 +1052,7 @@ __global__ void interp_generic_kernel(pif_soa_t P, const int32_t *__restrict__ p
             Q.x[i] = x; Q.y[i] = y; Q.z[i] = z;
             Q.vx[i] = vx; Q.vy[i] = vy; Q.vz[i] = vz;
             Q.id[i] = id;
-            const int kk = cell_key(x, y, z, pp.h, w, n);
+            const int kk = cell_key(x, y, z, pp.h, pp.rh, w, n);
             key[i] = kk;
             rank[i] = atomicAdd(&count[kk], 1);
         } else {
@@ -1162,6 +1167,14 @@ int persistent_blocks(K kernel, int threads, size_t smem, int sm_count) {
     return per_sm * sm_count;
 }
 
+// The DMMA kernels cover w <= 8; for w >= kPolyOnlyW they are compiled without
+// the exact-weight fallback, so a plan whose polynomials missed the bound there
+// (not the case for the reference's beta = 2.30 w) takes the generic kernels.
+bool fast_path_ok(const Plan &p) {
+    if (p.w > kMaxFastW || p.force_generic) return false;
+    return p.w < kPolyOnlyW || p.poly.exact_mask == 0;
+}
+
 PushParams make_push(const Plan &p, double half, double dt, const double *tq, const double *sq,
                      int has_b, int e_kind) {
     PushParams pp;
@@ -1169,6 +1182,12 @@ PushParams make_push(const Plan &p, double half, double dt, const double *tq, co
     pp.dt = dt;
     pp.L = p.L;
     pp.h = p.h;
+    pp.rh = 1.0 / p.h;
+    pp.ext_c = p.L / 2.0;       // the reference's constants (pif.py:52-57, 66-67)
+    pp.ext_xy = -15.0 / p.L;
+    pp.ext_z = 30.0 / p.L;
+    pp.pot_xy = 7.5 / p.L;
+    pp.pot_z = 15.0 / p.L;
     for (int d = 0; d < 3; ++d) {
         pp.tq[d] = tq ? tq[d] : 0.0;
         pp.sq[d] = sq ? sq[d] : 0.0;
@@ -1293,7 +1312,7 @@ int launch_spread(Plan &p, const pif_soa_t &P, const int32_t *perm, const double
     cudaError_t e = cudaMemsetAsync(p.grid, 0, sizeof(double) * p.n3, s);
     if (e != cudaSuccess) return fail_cuda(e, "zero grid");
     if (P.count == 0) return PIF_OK;
-    if (p.w <= kMaxFastW && !p.force_generic) {
+    if (fast_path_ok(p)) {
         const int nseg = (p.n + p.seg - 1) / p.seg;
         const int *nitems = p.seg_off + p.n_segs;
         e = cudaMemsetAsync(p.work, 0, sizeof(unsigned int), s);
@@ -1342,7 +1361,7 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
     const double4 *field = reinterpret_cast<const double4 *>(p.field);
     cudaError_t e;
     int blocks = 1;
-    if (P.count > 0 && p.w <= kMaxFastW && !p.force_generic) {
+    if (P.count > 0 && fast_path_ok(p)) {
         const int nseg = (p.n + p.seg - 1) / p.seg;
         const int *nitems = p.seg_off + p.n_segs;
         e = cudaMemsetAsync(p.work, 0, sizeof(unsigned int), s);

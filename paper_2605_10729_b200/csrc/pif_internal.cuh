@@ -122,7 +122,14 @@ __host__ __device__ inline int pmod(int i, int n) {
 
 // First stencil index and scaled coordinate for one axis, in the reference's
 // arithmetic: c = x / h (true division), i0 = ceil(c - w/2) (_kernels.py:19,74).
-__device__ __forceinline__ double axis_coord(double x, double h) { return __ddiv_rn(x, h); }
+// c = x / h correctly rounded, as the reference computes it (_kernels.py:41-43):
+// q = x * rh, rh = RN(1/h), corrected once by the exact residual x - q h
+// (Markstein: with a correctly rounded reciprocal and q within an ulp of x/h,
+// RN(q + r rh) = RN(x/h)).  Callers hoist rh = __drcp_rn(h) out of their loops.
+__device__ __forceinline__ double axis_coord(double x, double h, double rh) {
+    const double q = x * rh;
+    return fma(fma(-q, h, x), rh, q);
+}
 __device__ __forceinline__ double stencil_start(double c, int w) {
     return ceil(__dsub_rn(c, 0.5 * w));
 }
@@ -139,9 +146,18 @@ __device__ __forceinline__ double es_weight(double c, double i, double inv_half,
 
 __device__ __forceinline__ double wrap_coord(double x, double L) {
     // numpy float mod (sign follows the divisor) then the x == L guard
-    // (particles.py:65-70)
-    double r = fmod(x, L);
-    if (r != 0.0 && r < 0.0) r += L;
+    // (particles.py:65-70).  For x in [-L, 2L) np.mod is x, x - L (exact,
+    // Sterbenz) or x + L; anything farther takes the fmod route.
+    double r;
+    if (x >= 0.0 && x < L) return x;
+    if (x >= L && x < L + L) {
+        r = x - L;
+    } else if (x < 0.0 && x >= -L) {
+        r = x + L;
+    } else {
+        r = fmod(x, L);
+        if (r != 0.0 && r < 0.0) r += L;
+    }
     if (r >= L) r -= L;
     return r;
 }

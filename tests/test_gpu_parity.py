@@ -491,3 +491,30 @@ def test_cuda_graph_run_matches_eager(cuda):
     assert np.max(np.abs(a[:, :6] - b[:, :6]) / np.maximum(np.abs(a[:, :6]), 1e-300)) <= 1e-12
     ref = CFG["landau_trace"]
     assert np.max(np.abs(b[:21, 0] - ref[:, 2]) / ref[:, 2]) <= 1e-10
+
+
+def test_device_wrap_matches_numpy_mod_bitwise(cuda):
+    """pif_wrap_points == the reference's wrap_positions (np.mod + the == L guard,
+    particles.py:65-70) bit for bit, across the fast ranges and the fmod route."""
+    import torch
+    from paper_2605_10729_b200 import _native
+    L = 4 * np.pi
+    rng = np.random.default_rng(5)
+    tiny = np.nextafter(0.0, -1.0)
+    vals = np.concatenate([
+        rng.uniform(-L, 2 * L, 200000),                   # the three fast ranges
+        rng.uniform(-50 * L, 50 * L, 20000),              # fmod route
+        [0.0, -0.0, L, -L, 2 * L, -2 * L, np.nextafter(L, 0), np.nextafter(L, 3 * L),
+         np.nextafter(-L, 0), np.nextafter(2 * L, 0), tiny, -1e-300, 1e-300, 3 * L],
+    ])
+    ref = np.mod(vals, L)
+    ref[ref >= L] -= L
+    plan = pb.make_plan(16, L, 1e-7)
+    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    y, z = t.clone(), t.clone()
+    _native.call("pif_wrap_points", plan.native(t.device).handle, t.data_ptr(), y.data_ptr(),
+                 z.data_ptr(), t.numel(), _native.stream_handle(t.device))
+    got = t.cpu().numpy()
+    assert np.all((got >= 0) & (got < L))
+    same = (got == ref)
+    assert same.all(), vals[~same][:5]
