@@ -244,8 +244,12 @@ __device__ __forceinline__ void spread_flush_plane(double (&acc)[8][2], int k, i
     }
 }
 
+#ifndef PIF_SPREAD_MINB
+#define PIF_SPREAD_MINB 5
+#endif
+
 template <int W>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, PIF_SPREAD_MINB)
 spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
                   const double *__restrict__ pz, const int64_t *__restrict__ pid,
                   const int32_t *__restrict__ perm, const double *__restrict__ strengths, double q,
