@@ -347,8 +347,9 @@ def run_b200(a):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": a.warmup, "ms_per_step": T / K * 1e3, "higher_is_better": True,
             "scaling": a.scaling, "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (device sampler: Landau inverse-CDF / Penning Gaussian, "
-                    "N(0,1) velocities)",
+            "data": "synthetic: the reference's own seed-0 ensemble (bench.py Philox "
+                    "streams, Landau inverse-CDF / Penning rejection Gaussian, N(0,1) "
+                    "velocities) regenerated in HBM by the pif_sample_* kernels",
             "config": cfg, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk,
         }

@@ -185,6 +185,27 @@ int pif_type2_complex(pif_plan_t plan, const double *modes, const double *pts, i
  * iterations of 8 independent FMAs; *flops_out = flops issued. */
 int pif_probe_fp64(double *scratch, int blocks, int threads, int iters, void *stream,
                    double *flops_out);
+/* ---- device samplers (reference bench.py:67-122) -----
+ * One numpy Philox4x64-10 stream per (seed, attribute): counter[4] / key[2] as
+ * numpy's Philox(SeedSequence((seed, attr))).state holds them; uint64 number j
+ * of the stream is drawn for global index j.  Output element i goes to
+ * out[i * stride] (stride 3 writes one column of an (M, 3) array).  *status is
+ * OR-ed with 1 (CDF inversion failed) / 2 (rejection budget exhausted).
+ *
+ * Landau positions of ids [lo, lo + count): Newton inversion of
+ * (x + (alpha/k) sin kx)/L = u_id with bisection rescue, then wrapped
+ * (replaces _invert_landau_cdf + wrap_positions, bench.py:80-110,151-154). */
+int pif_sample_landau_axis(const uint64_t *counter, const uint64_t *key, int64_t lo,
+                           int64_t count, double alpha, double k, double L, double *out,
+                           int64_t stride, int *status, void *stream);
+/* Normals of ids [lo, lo + count) out of n_total: budget == 0 gives
+ * _standard_normal (Box-Muller of rows 0 / 1 of a (2, n_total) draw,
+ * bench.py:71-77); budget > 0 gives _rejection_normal_in_box, the first of
+ * mean + std * normal over rows r / budget + r (r < budget) inside [0, L)
+ * (bench.py:113-122). */
+int pif_sample_normal(const uint64_t *counter, const uint64_t *key, int64_t n_total, int64_t lo,
+                      int64_t count, double mean, double std_dev, int budget, double L,
+                      double *out, int64_t stride, int *status, void *stream);
 /* Profiling builds only (-DPIF_PHASE_TIMING): per-phase SM cycles of the
  * gather+push kernel summed over warps since the last call, out[0..4] =
  * {weights, DMMA gather, push, chunks, particles}; PIF_ERR_STATE otherwise. */

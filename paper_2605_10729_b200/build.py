@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libpifb200.so")
-SOURCES = ["particles.cu", "fields.cu", "capi.cu", "probe.cu"]
+SOURCES = ["particles.cu", "fields.cu", "capi.cu", "probe.cu", "sampler.cu"]
 HEADERS = ["pif_internal.cuh", "es_fast.cuh", os.path.join("..", "..", "include", "pif_b200.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -33,6 +33,42 @@ def test_samplers_bit_identical_to_reference(key):
     assert _sha(e.x, e.v, e.ids) == bytes(SAMP[key]).decode()
 
 
+_M64 = (1 << 64) - 1
+
+
+def _philox4x64_word(counter, key, j):
+    """Pure-Python Philox4x64-10 word j of a stream: the counter / round / key
+    schedule the device sampler (csrc/sampler.cu philox_word) implements."""
+    c = sum(int(counter[i]) << (64 * i) for i in range(4)) + 1 + (j >> 2)
+    c = [(c >> (64 * i)) & _M64 for i in range(4)]
+    k0, k1 = int(key[0]), int(key[1])
+    for r in range(10):
+        if r:
+            k0, k1 = (k0 + 0x9E3779B97F4A7C15) & _M64, (k1 + 0xBB67AE8584CAA73B) & _M64
+        p0, p1 = 0xD2E7470EE14C6C93 * c[0], 0xCA5A826395121157 * c[2]
+        c = [(p1 >> 64) ^ c[1] ^ k0, p1 & _M64, (p0 >> 64) ^ c[3] ^ k1, p0 & _M64]
+    return c[j & 3]
+
+
+@pytest.mark.parametrize("seed,attr", [(0, 0), (0, 5), (7, 2), (123456789, 4)])
+def test_device_sampler_stream_layout_matches_numpy(seed, attr):
+    """uint64 number j of the reference's (seed, attr) stream is word j & 3 of
+    Philox(counter0 + 1 + j // 4, key); uniforms are (raw >> 11) 2^-53."""
+    ctr, key = samplers.philox_state(seed, attr)
+    gen = np.random.Philox(np.random.SeedSequence((seed, attr)))
+    raw = gen.random_raw(23)
+    for j in (0, 1, 2, 3, 4, 7, 22):
+        assert _philox4x64_word(ctr, key, j) == int(raw[j])
+    u = samplers._stream(seed, attr).random(9)
+    assert all(u[j] == (int(raw[j]) >> 11) * 2.0 ** -53 for j in range(9))
+    # a 256-bit carry across the low counter word
+    big = np.array([_M64, 0, 0, 0], dtype=np.uint64)
+    gen.state = {"bit_generator": "Philox", "state": {"counter": big, "key": key},
+                 "buffer": np.zeros(4, dtype=np.uint64), "buffer_pos": 4, "has_uint32": 0,
+                 "uinteger": 0}
+    assert _philox4x64_word(big, key, 5) == int(gen.random_raw(6)[5])
+
+
 def test_id_slices_partition():
     for n_p, size in ((10, 3), (65536, 8), (7, 7), (5, 8)):
         spans = [samplers.id_slice(n_p, r, size) for r in range(size)]
