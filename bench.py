@@ -219,7 +219,7 @@ def run_b200(a):
     import paper_2605_10729_b200 as pb
     from paper_2605_10729_b200.comm import Comm, TorchDistTransport
     from paper_2605_10729_b200.engine import PifEngine
-    from paper_2605_10729_b200.samplers import id_slice, sample_device
+    from paper_2605_10729_b200.samplers import id_slice
 
     rank, world, local = dist_env()
     if world > 1:
@@ -238,10 +238,7 @@ def run_b200(a):
     m = abs(gspec.Q_e) / glob
     eng = PifEngine(plan, hi - lo, dev, q=q, m=m, externals=gspec.externals(), dt=a.dt,
                     comm=comm)
-    x, v, ids = sample_device(gspec, (lo, hi), dev)
-    eng.load(x, v, ids)
-    del x, v, ids
-    torch.cuda.empty_cache()
+    eng.load_sampled(gspec, (lo, hi))
 
     peak = fp64_peak_tflops(torch, dev)
 

@@ -112,6 +112,27 @@ class PifEngine:
                          self.parts.key.data_ptr(), self.parts.rank.data_ptr(), s)
             self._bin()
 
+    def load_sampled(self, spec, id_range, seed: int | None = None):
+        """Generate this rank's slice of the reference ensemble directly into the
+        SoA store (no AoS staging: 2^30 particles fit one GPU) and bin it."""
+        from .samplers import sample_device_into
+        lo, hi = id_range
+        if hi - lo != self.count:
+            raise ValueError(f"id range {id_range} does not hold {self.count} particles")
+        soa = self.parts.soa
+        sample_device_into(spec, id_range, [soa[d].data_ptr() for d in range(3)],
+                           [soa[3 + d].data_ptr() for d in range(3)], 1, self.device, seed)
+        torch = require_cuda()
+        ids = self.parts.ids[self.parts.cur]
+        torch.arange(lo, hi, dtype=torch.int64, device=self.device, out=ids[:self.count])
+        if self.count:
+            s = self._stream()
+            cur = self._soa()
+            _native.call("pif_wrap_points", self.handle, cur.x, cur.y, cur.z, self.count, s)
+            _native.call("pif_bin_keys", self.handle, ctypes.byref(cur),
+                         self.parts.key.data_ptr(), self.parts.rank.data_ptr(), s)
+            self._bin()
+
     def _bin(self):
         """Cell-ordered view: perm from the keys/ranks of the current buffer."""
         _native.call("pif_bin_perm", self.handle, self.parts.key.data_ptr(),

@@ -548,3 +548,28 @@ def test_device_sampler_reproduces_reference_ensemble(kind, cuda):
     rho = pb.deposit_charge(dev_ens, plan).coeffs
     rho = rho.cpu().numpy() if hasattr(rho, "cpu") else rho
     assert rel_l2(rho, CFG[f"{kind}_rho0"]) <= 1e-10
+
+
+def test_engine_load_sampled_equals_staged_load(cuda):
+    """PifEngine.load_sampled (sampling straight into the SoA store, the 2^30
+    path) gives the same binned particle set as load(sample_device(...))."""
+    import torch
+
+    from paper_2605_10729_b200.engine import PifEngine
+    from paper_2605_10729_b200.samplers import sample_device
+    spec = pb.penning_spec(N=16, ppm=8, seed=3)
+    n = spec.num_particles
+    lo, hi = 1000, n - 77
+    plan = pb.make_plan(spec.N, spec.L, 1e-7)
+    outs = []
+    for staged in (False, True):
+        eng = PifEngine(plan, hi - lo, "cuda", q=spec.Q_e / n, m=-spec.Q_e / n,
+                        externals=spec.externals(), dt=spec.dt)
+        if staged:
+            eng.load(*sample_device(spec, (lo, hi), "cuda"))
+        else:
+            eng.load_sampled(spec, (lo, hi))
+        x, v, ids = eng.parts.download(sort_by_id=True)
+        outs.append((x, v, ids))      # (perm order within a cell is atomic-order)
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)
