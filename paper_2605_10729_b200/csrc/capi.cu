@@ -202,6 +202,7 @@ int pif_plan_create(const pif_plan_desc_t *d, int device, pif_plan_t *out) {
     pif::build_es_poly(p.w, p.beta, &p.poly, &p.poly_err);
     if (const char *ws = std::getenv("PIF_INTERP_WS")) p.interp_ws = std::atoi(ws) != 0;
     if (const char *fg = std::getenv("PIF_FORCE_GENERIC")) p.force_generic = std::atoi(fg) != 0;
+    if (const char *st = std::getenv("PIF_SEG_TARGET")) p.seg_target = std::max(1, std::atoi(st));
     int rc = PIF_OK;
 #define TRY(x)                    \
     do {                          \

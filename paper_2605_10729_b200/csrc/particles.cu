@@ -287,6 +287,8 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
         int k = k0;
         int cell_end = cell_start[base + k0 + 1];
         while (cell_end <= pbeg) cell_end = cell_start[base + (++k) + 1];   // first cell
+        // end of the following cell, loaded one cell ahead (k + 2 <= n: cell_start has n3 + 1)
+        int next_end = cell_start[base + min(k + 2, k1)];
 
         double nx = 0.0, ny = 0.0, nz = 0.0, ns = q;
         if (pbeg + lane < pend) {
@@ -313,7 +315,8 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
                 if (gp >= cell_end) {
                     spread_flush_plane<W>(acc, k, c4, ix, yrow, n, grid);
                     ++k;
-                    cell_end = cell_start[base + k + 1];
+                    cell_end = next_end;
+                    next_end = cell_start[base + min(k + 2, k1)];
                     continue;
                 }
                 const int m = min(4, min(pos + cnt, cell_end) - gp);
@@ -1249,7 +1252,20 @@ static EsPoly device_poly(const Plan &p) {
     return e;
 }
 
+// Cells per z-segment work item: 8 at the benchmark density (64 particles per
+// stencil cell); sparser sets get longer segments (up to 31, the gather's
+// one-lane-per-cell start table) so an item still holds ~seg_target particles
+// and the per-item window / first-chunk loads stay amortised.
+int segment_cells(const Plan &p, int64_t M) {
+    const double per_cell = (double)M / (double)p.n3;
+    const double want = (double)p.seg_target / (per_cell > 1.0 ? per_cell : 1.0);
+    const int seg = (int)std::ceil(want);
+    return seg < 8 ? 8 : (seg > 31 ? 31 : seg);
+}
+
 int build_items(Plan &p, int64_t M, cudaStream_t s) {
+    p.seg = segment_cells(p, M);
+    p.n_segs = p.n * p.n * ((p.n + p.seg - 1) / p.seg);
     const int64_t need = p.n_segs + M / kItemParticles + 1;
     if (need > p.items_cap) {
         if (p.items) cudaFree(p.items);

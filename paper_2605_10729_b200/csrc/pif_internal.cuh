@@ -41,7 +41,8 @@ struct Plan {
     int N = 0, n = 0, w = 0, device = 0;
     double L = 0, eps = 0, beta = 0, h = 0, inv_L3 = 0, half_L3 = 0;
     int64_t n3 = 0, nhalf = 0;     // n^3, n*n*(n/2+1)
-    int seg = 8;                   // cells per z-segment work item
+    int seg = 8;                   // cells per z-segment work item (set per binning)
+    int seg_target = 512;          // particles per work item the segment length aims at
     double *deconv = nullptr;      // (N,)
     double *kvec = nullptr;        // (N,) 2 pi m / L
     double *grid = nullptr;        // n^3 real fine grid
