@@ -244,8 +244,12 @@ __device__ __forceinline__ void spread_flush_plane(double (&acc)[8][2], int k, i
     }
 }
 
+#ifndef PIF_SPREAD_UNROLL
+#define PIF_SPREAD_UNROLL 2
+#endif
+constexpr int kSpreadUnroll = PIF_SPREAD_UNROLL;
 #ifndef PIF_SPREAD_MINB
-#define PIF_SPREAD_MINB 5
+#define PIF_SPREAD_MINB 4
 #endif
 
 template <int W>
@@ -311,23 +315,37 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
             chunk_weights<W, false>(st, tab, poly, lane, cnt, cx, cy, cz, cs, true, h, rh, beta);
             int j = 0;
             while (j < cnt) {
-                const int gp = pos + j;
-                if (gp >= cell_end) {
+                if (pos + j >= cell_end) {
                     spread_flush_plane<W>(acc, k, c4, ix, yrow, n, grid);
                     ++k;
                     cell_end = next_end;
                     next_end = cell_start[base + min(k + 2, k1)];
                     continue;
                 }
-                const int m = min(4, min(pos + cnt, cell_end) - gp);
-                const bool ok = c4 < m;
-                const int pj = ok ? j + c4 : j;
-                PIF_CHECK(m > 0 && pj < kChunk && k >= k0 && k < k1);
-                const double wyb = ok ? st.wy[pj][r] : 0.0;
-                const double bz = st.wz[pj][(r - k) & 7];
+                const int jend = min(cnt, cell_end - pos);   // this cell's part of the chunk
+                const int zs = (r - k) & 7;
+                PIF_CHECK(jend <= kChunk && k >= k0 && k < k1);
+                // full k-steps of 4 particles: no masking, unrolled so the next
+                // step's shared-memory loads overlap this step's DMMAs
+#pragma unroll kSpreadUnroll
+                for (; j + 4 <= jend; j += 4) {
+                    const int pj = j + c4;
+                    const double wyb = st.wy[pj][r];
+                    const double bz = st.wz[pj][zs];
 #pragma unroll
-                for (int a = 0; a < 8; ++a) dmma884(acc[a][0], acc[a][1], st.wx[a][pj] * wyb, bz);
-                j += m;
+                    for (int a = 0; a < 8; ++a)
+                        dmma884(acc[a][0], acc[a][1], st.wx[a][pj] * wyb, bz);
+                }
+                if (j < jend) {   // ragged tail of the cell
+                    const bool ok = c4 < jend - j;
+                    const int pj = ok ? j + c4 : j;
+                    const double wyb = ok ? st.wy[pj][r] : 0.0;
+                    const double bz = st.wz[pj][zs];
+#pragma unroll
+                    for (int a = 0; a < 8; ++a)
+                        dmma884(acc[a][0], acc[a][1], st.wx[a][pj] * wyb, bz);
+                    j = jend;
+                }
             }
             __syncwarp();
         }
