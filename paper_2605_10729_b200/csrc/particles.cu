@@ -165,6 +165,12 @@ struct WarpChunk {
     double E[3][kChunk];        // gathered field (gather+push)
 };
 
+// gather: per-particle partial sums over (a, c) for each y offset b, reduced
+// against wy in the push phase instead of a shuffle tree per sub-batch
+struct GatherPartials {
+    double D[3][kChunk][9];     // [component][p][b]
+};
+
 __device__ __forceinline__ void chunk_zero(WarpChunk &st, int lane) {
     double *w = &st.wx[0][0];
     const int nw = 8 * (kChunk + 1) + 2 * kChunk * 9;
@@ -519,6 +525,61 @@ __device__ __forceinline__ void gather_sub(WarpChunk &st, const double (&g)[8][2
     }
 }
 
+// As gather_sub, but the 8 x 8 result D_d[p][b] of the sub-batch goes to
+// shared memory; E_d(p) = sum_b wy_p[b] D_d[p][b] is formed later by lane p
+// (gather_reduce), off the DMMA loop's critical path.
+__device__ __forceinline__ void gather_sub_d(WarpChunk &st, GatherPartials &gp,
+                                             const double (&g)[8][2][3], int j, int m, int k,
+                                             int r, int c4) {
+    const int pb = r < m ? j + r : j;
+    const double sc = r < m ? 1.0 : 0.0;
+    const double bz0 = sc * st.wz[pb][(c4 - k) & 7];
+    const double bz1 = sc * st.wz[pb][(c4 + 4 - k) & 7];
+    double A[8][2];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+        const double wxa = st.wx[a][pb];
+        A[a][0] = wxa * bz0;
+        A[a][1] = wxa * bz1;
+    }
+    double Dh[2][3][2];
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) Dh[hh][d][0] = Dh[hh][d][1] = 0.0;
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+            for (int d = 0; d < 3; ++d)
+                dmma884(Dh[hh][d][0], Dh[hh][d][1], A[a][hh], g[a][hh][d]);
+    if (r < m) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            gp.D[d][j + r][2 * c4] = Dh[0][d][0] + Dh[1][d][0];
+            gp.D[d][j + r][2 * c4 + 1] = Dh[0][d][1] + Dh[1][d][1];
+        }
+    }
+}
+
+// E of this lane's particle p from its partial sums (same pairing as the
+// shuffle tree of gather_sub: ((b0 b1 + b2 b3) + (b4 b5 + b6 b7)))
+__device__ __forceinline__ void gather_reduce(const WarpChunk &st, const GatherPartials &gp, int p,
+                                              double (&E)[3]) {
+    double wy[8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) wy[b] = st.wy[p][b];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        double e[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            e[q] = fma(wy[2 * q + 1], gp.D[d][p][2 * q + 1], wy[2 * q] * gp.D[d][p][2 * q]);
+        E[d] = (e[0] + e[1]) + (e[2] + e[3]);
+    }
+}
+
 // Next-plane prefetch: all 32 lanes copy the 8 x 8 double4 block of plane z
 // into shared memory with cp.async (LDGSTS) one cell ahead of its use.
 __device__ __forceinline__ void prefetch_plane(double4 (*pf)[8], const double4 *field, int ix,
@@ -845,6 +906,9 @@ interp_ws_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
 #ifndef PIF_INTERP_MINB
 #define PIF_INTERP_MINB 2
 #endif
+#ifndef PIF_GATHER_DEFER
+#define PIF_GATHER_DEFER 1
+#endif
 
 template <int W, bool PUSH>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, PIF_INTERP_MINB)
@@ -859,6 +923,10 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
     __shared__ WarpChunk stage[kWarpsPerBlock];
     __shared__ double4 planes[kWarpsPerBlock][8][8];
     __shared__ double tab[32];
+#if PIF_GATHER_DEFER
+    extern __shared__ double4 dyn_smem[];
+    GatherPartials &gpart = reinterpret_cast<GatherPartials *>(dyn_smem)[threadIdx.x >> 5];
+#endif
     if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -951,7 +1019,11 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                 }
                 const int m = min(8, min(pos + cnt, cell_end) - gp);
                 PIF_CHECK(m > 0 && j + m <= kChunk && k >= k0 && k < k1);
+#if PIF_GATHER_DEFER
+                gather_sub_d(st, gpart, g, j, m, k, r, c4);
+#else
                 gather_sub(st, g, j, m, k, r, c4);
+#endif
                 j += m;
             }
             __syncwarp();
@@ -959,7 +1031,13 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
             PHASE_ADD(1, t1, t2);
             if (lane < cnt) {
                 const int64_t i = pos + lane;
+#if PIF_GATHER_DEFER
+                double Eg[3];
+                gather_reduce(st, gpart, lane, Eg);
+                const double E0 = Eg[0], E1 = Eg[1], E2 = Eg[2];
+#else
                 const double E0 = st.E[0][lane], E1 = st.E[1][lane], E2 = st.E[2][lane];
+#endif
                 if (PUSH) {
                     double x = x0, y = y0, z = z0;
                     double vx = vx0, vy = vy0, vz = vz0;
@@ -1386,6 +1464,9 @@ int launch_spread(Plan &p, const pif_soa_t &P, const int32_t *perm, const double
     return fail_cuda(cudaGetLastError(), "spread kernel");
 }
 
+// dynamic shared memory of interp_mma_kernel: the per-warp partial sums
+constexpr int kGatherDyn = PIF_GATHER_DEFER ? (int)(kWarpsPerBlock * sizeof(GatherPartials)) : 0;
+
 int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q, bool push,
                   double half, double dt, const double *tq, const double *sq, int has_b,
                   int e_kind, int32_t *key, int32_t *rank, double *diag, double *E_out,
@@ -1416,16 +1497,20 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
                                     nitems);                                                  \
         } else if (push) {                                                                    \
             auto k = interp_mma_kernel<W, true>;                                             \
-            blocks = persistent_blocks(k, threads, 0, p.sm_count);                            \
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kGatherDyn);  \
+            blocks = persistent_blocks(k, threads, kGatherDyn, p.sm_count);                   \
             if (blocks > p.partial_blocks) blocks = p.partial_blocks;                         \
-            k<<<blocks, threads, 0, s>>>(P, perm, Q, p.cell_start, field, p.seg, nseg, p.beta,   \
+            k<<<blocks, threads, kGatherDyn, s>>>(P, perm, Q, p.cell_start, field, p.seg, nseg,  \
+                                                  p.beta,                                     \
                                          poly, pp,                                            \
                                          key, rank, p.cell_count, p.partials, E_out, p.work,   \
                                          p.items, nitems);                                    \
         } else {                                                                              \
             auto k = interp_mma_kernel<W, false>;                                            \
-            blocks = persistent_blocks(k, threads, 0, p.sm_count);                            \
-            k<<<blocks, threads, 0, s>>>(P, perm, Q, p.cell_start, field, p.seg, nseg, p.beta,   \
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kGatherDyn);  \
+            blocks = persistent_blocks(k, threads, kGatherDyn, p.sm_count);                   \
+            k<<<blocks, threads, kGatherDyn, s>>>(P, perm, Q, p.cell_start, field, p.seg, nseg,  \
+                                                  p.beta,                                     \
                                          poly, pp,                                            \
                                          key, rank, p.cell_count, p.partials, E_out, p.work,   \
                                          p.items, nitems);                                    \
