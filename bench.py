@@ -366,36 +366,20 @@ def run_e2e(a, eng, torch, dist, world, per_gpu, glob, dev):
     lo = int(eng.parts.ids[eng.parts.cur][:M].min())
     xh = torch.empty((M, 3), dtype=torch.float64, pin_memory=True)
     vh = torch.empty((M, 3), dtype=torch.float64, pin_memory=True)
-    wo = torch.empty(1, dtype=torch.float64, pin_memory=True)
-    xd = torch.empty((M, 3), dtype=torch.float64, device=dev)
-    vd = torch.empty((M, 3), dtype=torch.float64, device=dev)
-    idd = torch.arange(lo, lo + M, dtype=torch.int64, device=dev)
-    eng.to_id_order(xd, vd, lo)
+    xd, vd = eng.to_id_order(id0=lo)
     xh.copy_(xd)
     vh.copy_(vd)
+    del xd, vd
 
-    def one():
-        xd.copy_(xh, non_blocking=True)
-        vd.copy_(vh, non_blocking=True)
-        eng.load(xd, vd, idd)
-        eng.deposit()
-        eng.allreduce()
-        eng.solve_fields()
-        eng.gather_push()
-        eng.to_id_order(xd, vd, lo)
-        xh.copy_(xd, non_blocking=True)   # the host arrays hold the state
-        vh.copy_(vd, non_blocking=True)
-        wo.copy_(eng.scalars[0:1], non_blocking=True)
-
-    one()
+    wh = torch.empty(max(1, a.e2e_steps), dtype=torch.float64, pin_memory=True)
+    eng.run_host(xh, vh, lo, 1, energy_out=wh)       # warm-up (allocates the staging)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     K = max(1, a.e2e_steps)
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
-    for _ in range(K):
-        one()
+    eng.run_host(xh, vh, lo, K, energy_out=wh)
     e.record()
     torch.cuda.synchronize(dev)
     T = s.elapsed_time(e) * 1e-3
@@ -405,8 +389,9 @@ def run_e2e(a, eng, torch, dist, world, per_gpu, glob, dev):
         T = float(tt[0])
     return {"value": glob * K / T, "unit": UNIT, "h2d_bytes_per_step": M * 48 * world,
             "d2h_bytes_per_step": (M * 48 + 8) * world, "steps": K,
-            "api": "pif_step-style: host pinned x,v (id order) -> PifEngine.load -> deposit -> "
-                   "allreduce -> solve_fields -> gather_push -> id-order scatter -> D2H x,v,W"}
+            "api": "PifEngine.run_host (pif_step-style): per step H2D x,v (pinned, id order) -> "
+                   "load/bin -> deposit -> allreduce -> solve_fields -> gather_push -> id-order "
+                   "scatter -> D2H x,v,W; step s's D2H and step s+1's H2D chunk-pipelined"}
 
 
 def main():

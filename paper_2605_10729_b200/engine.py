@@ -287,6 +287,62 @@ class PifEngine:
         self.allreduce()
         self.solve_fields()
 
+    def run_host(self, xh, vh, id0: int, steps: int, energy_out=None, n_chunks: int = 16):
+        """pif_step-style stepping of a host-resident ensemble (the reference's
+        ParticleEnsemble use, pif.py:178-190): every step uploads x, v ((M,3),
+        id order, ids id0 .. id0+M-1) from host memory, bins, deposits, reduces,
+        solves, gathers + pushes, scatters back to id order and downloads x, v
+        into the same host arrays (energy_out[s] <- the step's field energy).
+
+        Copies run on two side streams.  The download of step s and the upload
+        of step s+1 read and write the same host arrays, so they are pipelined
+        chunk by chunk (each chunk's upload waits for its download): the two
+        PCIe directions overlap instead of running back to back.  Pin xh / vh
+        (torch pin_memory) for asynchronous copies."""
+        torch = require_cuda()
+        M, dev = self.count, self.device
+        if tuple(xh.shape) != (M, 3) or tuple(vh.shape) != (M, 3):
+            raise ValueError(f"host arrays must be ({M}, 3)")
+        main = torch.cuda.current_stream(dev)
+        down, up = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        if getattr(self, "_stage", None) is None or self._stage[0].shape[0] != M:
+            f64 = dict(dtype=torch.float64, device=dev)
+            self._stage = (torch.empty((M, 3), **f64), torch.empty((M, 3), **f64))
+        xd, vd = self._stage
+        ids = torch.arange(id0, id0 + M, dtype=torch.int64, device=dev)
+        step = max(1, -(-M // max(1, n_chunks)))
+        bounds = [(i, min(M, i + step)) for i in range(0, M, step)]
+        up.wait_stream(main)
+        with torch.cuda.stream(up):
+            xd.copy_(xh, non_blocking=True)
+            vd.copy_(vh, non_blocking=True)
+        for s in range(steps):
+            main.wait_stream(up)
+            self.load(xd, vd, ids)
+            self.deposit()
+            self.allreduce()
+            self.solve_fields()
+            self.gather_push()
+            self.to_id_order(xd, vd, id0)
+            if energy_out is not None:
+                energy_out[s:s + 1].copy_(self.scalars[0:1], non_blocking=True)
+            down.wait_stream(main)
+            last = s == steps - 1
+            for i0, i1 in bounds:
+                with torch.cuda.stream(down):
+                    xh[i0:i1].copy_(xd[i0:i1], non_blocking=True)
+                    vh[i0:i1].copy_(vd[i0:i1], non_blocking=True)
+                if not last:
+                    up.wait_stream(down)
+                    with torch.cuda.stream(up):
+                        xd[i0:i1].copy_(xh[i0:i1], non_blocking=True)
+                        vd[i0:i1].copy_(vh[i0:i1], non_blocking=True)
+        main.wait_stream(down)
+        main.wait_stream(up)
+        for t in (xd, vd, ids):
+            t.record_stream(down)
+            t.record_stream(up)
+
     def to_id_order(self, x_out=None, v_out=None, id0: int = 0):
         """(M,3) x, v in id order (ids id0 .. id0+M-1) via a device scatter."""
         torch = require_cuda()

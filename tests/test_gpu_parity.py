@@ -573,3 +573,27 @@ def test_engine_load_sampled_equals_staged_load(cuda):
         outs.append((x, v, ids))      # (perm order within a cell is atomic-order)
     for a, b in zip(outs[0], outs[1]):
         assert torch.equal(a, b)
+
+
+def test_run_host_streaming_matches_pif_step(cuda):
+    """PifEngine.run_host (host-resident x, v, chunk-pipelined copies) steps
+    exactly like repeated pif_step calls on the same ensemble."""
+    import torch
+
+    from paper_2605_10729_b200.engine import PifEngine
+    spec, ens = _config1("penning")
+    plan = pb.make_plan(spec.N, spec.L, 1e-7)
+    steps = 3
+    xh = torch.tensor(ens.x, dtype=torch.float64).pin_memory()
+    vh = torch.tensor(ens.v, dtype=torch.float64).pin_memory()
+    wh = torch.zeros(steps, dtype=torch.float64).pin_memory()
+    eng = PifEngine(plan, ens.count, "cuda", q=ens.q_per_particle, m=ens.m_per_particle,
+                    externals=spec.externals(), dt=spec.dt)
+    eng.run_host(xh, vh, 0, steps, energy_out=wh, n_chunks=7)
+    torch.cuda.synchronize()
+    st = pb.StepState(ensemble=ens.copy(), plan=plan, externals=spec.externals(), dt=spec.dt)
+    for _ in range(steps):
+        st = pb.pif_step(st)
+    assert rel_max(xh.numpy(), st.ensemble.x) <= 1e-12
+    assert rel_max(vh.numpy(), st.ensemble.v) <= 1e-12
+    assert np.all(np.isfinite(wh.numpy())) and np.all(wh.numpy() > 0)
