@@ -168,6 +168,20 @@ int pif_interp_perm(pif_plan_t plan, const pif_soa_t *parts, const int32_t *perm
  * id0 .. id0+M-1); v_out may be NULL. */
 int pif_soa_to_aos(pif_plan_t plan, const pif_soa_t *parts, int64_t id0, double *x_out,
                    double *v_out, void *stream);
+/* Host-layout (ParticleEnsemble, particles.py:10-62) streaming, used when the
+ * caller keeps the particles in host memory between steps (pif_step,
+ * pif.py:178-190):
+ * pif_load_aos: (M,3) AoS x, v rows of ids id0 .. id0+M-1 (device copies of the
+ * host arrays) -> wrapped SoA store dst (dst->count = M) with ids, cell keys and
+ * ranks in one pass (= upload + pif_wrap_points + pif_bin_keys); follow with
+ * pif_bin_perm.
+ * pif_set_id_order_output: while x_out/v_out are set, every pif_interp_push*
+ * launch also writes each pushed particle's x, v to row id - id0 of these (M,3)
+ * arrays (a fused pif_soa_to_aos); NULL, NULL clears.  Plan state: set it only
+ * around the pushes that should mirror. */
+int pif_load_aos(pif_plan_t plan, const double *x, const double *v, int64_t id0, pif_soa_t *dst,
+                 int32_t *key, int32_t *rank, void *stream);
+int pif_set_id_order_output(pif_plan_t plan, double *x_out, double *v_out, int64_t id0);
 /* Diagnostic sums of a particle set (Recorder.record, strategies.py:96-106). */
 int pif_particle_diag(pif_plan_t plan, const pif_soa_t *p, int e_kind, double *diag,
                       void *stream);

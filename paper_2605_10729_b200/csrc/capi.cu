@@ -464,6 +464,23 @@ int pif_soa_to_aos(pif_plan_t plan, const pif_soa_t *parts, int64_t id0, double 
     return pif::launch_soa_to_aos(p, *parts, id0, x_out, v_out, s);
 }
 
+int pif_set_id_order_output(pif_plan_t plan, double *x_out, double *v_out, int64_t id0) {
+    if (!plan) return pif::bad("null plan");
+    if ((x_out == nullptr) != (v_out == nullptr)) return pif::bad("x_out and v_out go together");
+    plan->p.mirror_x = x_out;
+    plan->p.mirror_v = v_out;
+    plan->p.mirror_id0 = id0;
+    return PIF_OK;
+}
+
+int pif_load_aos(pif_plan_t plan, const double *x, const double *v, int64_t id0, pif_soa_t *dst,
+                 int32_t *key, int32_t *rank, void *stream) {
+    PLAN_CHECK();
+    if (!pif::soa_ok(dst, true)) return pif::bad("invalid destination view");
+    if (dst->count > 0 && (!x || !v || !key || !rank)) return pif::bad("missing input / key / rank");
+    return pif::launch_load_aos(p, x, v, id0, *dst, key, rank, s);
+}
+
 int pif_particle_diag(pif_plan_t plan, const pif_soa_t *ps, int e_kind, double *diag,
                       void *stream) {
     PLAN_CHECK();

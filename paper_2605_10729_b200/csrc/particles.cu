@@ -101,6 +101,31 @@ __global__ void soa_to_aos_by_id_kernel(pif_soa_t P, int64_t id0, double *__rest
     }
 }
 
+// Host-layout upload in one pass (replaces upload + pif_wrap_points +
+// pif_bin_keys for ParticleEnsemble-shaped input): AoS (M,3) x, v rows in id
+// order -> wrapped SoA store, ids id0 + i, cell keys and ranks.
+__global__ void load_aos_kernel(const double *__restrict__ xa, const double *__restrict__ va,
+                                int64_t id0, int64_t M, pif_soa_t dst, double L, double h,
+                                int w, int n, int32_t *__restrict__ key,
+                                int32_t *__restrict__ rank, int32_t *__restrict__ count) {
+    const double rh = __drcp_rn(h);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double x = wrap_coord(xa[3 * i], L), y = wrap_coord(xa[3 * i + 1], L),
+                     z = wrap_coord(xa[3 * i + 2], L);
+        dst.x[i] = x;
+        dst.y[i] = y;
+        dst.z[i] = z;
+        dst.vx[i] = va[3 * i];
+        dst.vy[i] = va[3 * i + 1];
+        dst.vz[i] = va[3 * i + 2];
+        dst.id[i] = id0 + i;
+        const int k = cell_key(x, y, z, h, rh, w, n);
+        key[i] = k;
+        rank[i] = atomicAdd(&count[k], 1);
+    }
+}
+
 // perm[start[key[j]] + rank[j]] = j: the cell-ordered view of a particle set
 __global__ void bin_perm_kernel(const int32_t *__restrict__ key, const int32_t *__restrict__ rank,
                                 const int32_t *__restrict__ start, int64_t M,
@@ -388,7 +413,23 @@ struct PushParams {
     double ext_c, ext_xy, ext_z, pot_xy, pot_z;   // L/2, -15/L, 30/L, 7.5/L, 15/L
     double tq[3], sq[3];
     int has_b, e_kind, n, w;
+    double *mx, *mv;      // id-order mirror (pif_set_id_order_output) or null
+    long long mid0;
 };
+
+// pushed particle also written to row id - mid0 of the (M,3) mirrors
+__device__ __forceinline__ void mirror_store(const PushParams &pp, int64_t id, double x, double y,
+                                             double z, double vx, double vy, double vz) {
+    if (pp.mx) {
+        const int64_t o = 3 * (id - pp.mid0);
+        pp.mx[o] = x;
+        pp.mx[o + 1] = y;
+        pp.mx[o + 2] = z;
+        pp.mv[o] = vx;
+        pp.mv[o + 1] = vy;
+        pp.mv[o + 2] = vz;
+    }
+}
 
 // Boris push of one particle (pif.py:146-157), external quadrupole
 // (pif.py:52-57), periodic wrap (particles.py:65-70); no FMA contraction so the
@@ -969,7 +1010,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
             const int i = perm ? perm[pbeg + lane] : pbeg + lane;
             nx = P.x[i]; ny = P.y[i]; nz = P.z[i];
             if (PUSH) { nvx = P.vx[i]; nvy = P.vy[i]; nvz = P.vz[i]; }
-            if (perm || !PUSH) nid = P.id[i];
+            if (perm || !PUSH || pp.mx) nid = P.id[i];
         }
         // window: slot s = c4 + 4h holds plane z == s (mod 8) of [kf, kf+8)
         double g[8][2][3];
@@ -995,7 +1036,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                 const int i = perm ? perm[pos + kChunk + lane] : pos + kChunk + lane;
                 nx = P.x[i]; ny = P.y[i]; nz = P.z[i];
                 if (PUSH) { nvx = P.vx[i]; nvy = P.vy[i]; nvz = P.vz[i]; }
-                if (perm || !PUSH) nid = P.id[i];
+                if (perm || !PUSH || pp.mx) nid = P.id[i];
             }
             PHASE_MARK(t0);
             chunk_weights<W, true>(st, tab, poly, lane, cnt, x0, y0, z0, 1.0, false, h, pp.rh, beta);
@@ -1045,6 +1086,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                     Q.x[i] = x; Q.y[i] = y; Q.z[i] = z;
                     Q.vx[i] = vx; Q.vy[i] = vy; Q.vz[i] = vz;
                     if (perm) Q.id[i] = id0;
+                    mirror_store(pp, id0, x, y, z, vx, vy, vz);
                     const int kk = cell_key(x, y, z, h, pp.rh, pp.w, n);
                     PIF_CHECK(kk >= 0 && kk < n * n * n && i < P.count);
                     key[i] = kk;
@@ -1155,6 +1197,7 @@ __global__ void interp_generic_kernel(pif_soa_t P, const int32_t *__restrict__ p
             Q.x[i] = x; Q.y[i] = y; Q.z[i] = z;
             Q.vx[i] = vx; Q.vy[i] = vy; Q.vz[i] = vz;
             Q.id[i] = id;
+            mirror_store(pp, id, x, y, z, vx, vy, vz);
             const int kk = cell_key(x, y, z, pp.h, pp.rh, w, n);
             key[i] = kk;
             rank[i] = atomicAdd(&count[kk], 1);
@@ -1299,6 +1342,9 @@ PushParams make_push(const Plan &p, double half, double dt, const double *tq, co
     pp.e_kind = e_kind;
     pp.n = p.n;
     pp.w = p.w;
+    pp.mx = p.mirror_x;
+    pp.mv = p.mirror_v;
+    pp.mid0 = p.mirror_id0;
     return pp;
 }
 
@@ -1404,6 +1450,14 @@ int debug_phase_cycles(unsigned long long *out) {
 #endif
 }
 
+int launch_load_aos(Plan &p, const double *x, const double *v, int64_t id0, pif_soa_t &dst,
+                    int32_t *key, int32_t *rank, cudaStream_t s) {
+    if (dst.count == 0) return PIF_OK;
+    load_aos_kernel<<<grid_for(dst.count, 256, p.sm_count), 256, 0, s>>>(
+        x, v, id0, dst.count, dst, p.L, p.h, p.w, p.n, key, rank, p.cell_count);
+    return fail_cuda(cudaGetLastError(), "load_aos_kernel");
+}
+
 int launch_bin_perm(Plan &p, const int32_t *key, const int32_t *rank, int64_t M, int32_t *perm,
                     cudaStream_t s) {
     size_t tmp = p.scan_tmp_bytes;
@@ -1488,7 +1542,7 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
         const int threads = kWarpsPerBlock * 32;
 #define PIF_INTERP_CASE(W)                                                                    \
     case W: {                                                                                 \
-        if (push && p.interp_ws) {                                                            \
+        if (push && p.interp_ws && !pp.mx) {                                                  \
             auto k = interp_ws_kernel<W>;                                                     \
             blocks = persistent_blocks(k, 64, 0, p.sm_count);                                 \
             if (blocks > p.partial_blocks) blocks = p.partial_blocks;                         \

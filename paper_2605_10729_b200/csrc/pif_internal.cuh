@@ -43,6 +43,9 @@ struct Plan {
     int64_t n3 = 0, nhalf = 0;     // n^3, n*n*(n/2+1)
     int seg = 8;                   // cells per z-segment work item (set per binning)
     int seg_target = 512;          // particles per work item the segment length aims at
+    double *mirror_x = nullptr;    // id-order (M,3) mirrors written by the push kernels
+    double *mirror_v = nullptr;
+    long long mirror_id0 = 0;
     double *deconv = nullptr;      // (N,)
     double *kvec = nullptr;        // (N,) 2 pi m / L
     double *grid = nullptr;        // n^3 real fine grid
@@ -95,6 +98,8 @@ int launch_bin_perm(Plan &p, const int32_t *key, const int32_t *rank, int64_t M,
                     cudaStream_t s);
 int launch_spread(Plan &p, const pif_soa_t &parts, const int32_t *perm, const double *strengths,
                   double q, cudaStream_t s);
+int launch_load_aos(Plan &p, const double *x, const double *v, int64_t id0, pif_soa_t &dst,
+                    int32_t *key, int32_t *rank, cudaStream_t s);
 int launch_interp(Plan &p, const pif_soa_t &src, const int32_t *perm, pif_soa_t &dst, bool push,
                   double half, double dt, const double *tq, const double *sq, int has_b,
                   int e_kind, int32_t *key, int32_t *rank, double *diag, double *E_out,

@@ -112,6 +112,17 @@ class PifEngine:
                          self.parts.key.data_ptr(), self.parts.rank.data_ptr(), s)
             self._bin()
 
+    def load_aos(self, x, v, id0: int):
+        """Device (M,3) AoS x, v of ids id0 .. id0+M-1 (host ParticleEnsemble
+        layout) -> SoA store, wrapped, binned: one fused pass + perm."""
+        if self.count:
+            cur = self._soa()
+            _native.call("pif_load_aos", self.handle, x.data_ptr(), v.data_ptr(), int(id0),
+                         ctypes.byref(cur), self.parts.key.data_ptr(),
+                         self.parts.rank.data_ptr(), self._stream())
+            self.launches += 1
+            self._bin()
+
     def load_sampled(self, spec, id_range, seed: int | None = None):
         """Generate this rank's slice of the reference ensemble directly into the
         SoA store (no AoS staging: 2^30 particles fit one GPU) and bin it."""
@@ -309,7 +320,6 @@ class PifEngine:
             f64 = dict(dtype=torch.float64, device=dev)
             self._stage = (torch.empty((M, 3), **f64), torch.empty((M, 3), **f64))
         xd, vd = self._stage
-        ids = torch.arange(id0, id0 + M, dtype=torch.int64, device=dev)
         step = max(1, -(-M // max(1, n_chunks)))
         bounds = [(i, min(M, i + step)) for i in range(0, M, step)]
         up.wait_stream(main)
@@ -318,12 +328,17 @@ class PifEngine:
             vd.copy_(vh, non_blocking=True)
         for s in range(steps):
             main.wait_stream(up)
-            self.load(xd, vd, ids)
+            self.load_aos(xd, vd, id0)
             self.deposit()
             self.allreduce()
             self.solve_fields()
-            self.gather_push()
-            self.to_id_order(xd, vd, id0)
+            # the push also writes x, v in id order into the staging arrays
+            _native.call("pif_set_id_order_output", self.handle, xd.data_ptr(), vd.data_ptr(),
+                         int(id0))
+            try:
+                self.gather_push()
+            finally:
+                _native.call("pif_set_id_order_output", self.handle, None, None, 0)
             if energy_out is not None:
                 energy_out[s:s + 1].copy_(self.scalars[0:1], non_blocking=True)
             down.wait_stream(main)
@@ -339,7 +354,7 @@ class PifEngine:
                         vd[i0:i1].copy_(vh[i0:i1], non_blocking=True)
         main.wait_stream(down)
         main.wait_stream(up)
-        for t in (xd, vd, ids):
+        for t in (xd, vd):
             t.record_stream(down)
             t.record_stream(up)
 
