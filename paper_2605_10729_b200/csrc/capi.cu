@@ -54,7 +54,7 @@ int dalloc(Plan &p, T **ptr, size_t count) {
 void release(Plan &p) {
     void *ptrs[] = {p.deconv, p.kvec, p.grid, p.spec, p.field, p.field3, p.emodes, p.cgrid,
                     p.cell_count, p.cell_start, p.scan_tmp, p.work, p.partials, p.maxbits,
-                    p.shape_tab};
+                    p.shape_tab, p.items, p.seg_parts, p.seg_off, p.ring_scratch};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     if (p.d2z) cufftDestroy(p.d2z);
@@ -203,6 +203,7 @@ int pif_plan_create(const pif_plan_desc_t *d, int device, pif_plan_t *out) {
     if (const char *ws = std::getenv("PIF_INTERP_WS")) p.interp_ws = std::atoi(ws) != 0;
     if (const char *fg = std::getenv("PIF_FORCE_GENERIC")) p.force_generic = std::atoi(fg) != 0;
     if (const char *st = std::getenv("PIF_SEG_TARGET")) p.seg_target = std::max(1, std::atoi(st));
+    if (const char *fr = std::getenv("PIF_FORCE_RING")) p.force_ring = std::atoi(fr) != 0;
     int rc = PIF_OK;
 #define TRY(x)                    \
     do {                          \
@@ -305,7 +306,7 @@ int pif_debug_phase_cycles(unsigned long long *out) {
 }
 
 int pif_es_poly_info(int w, double beta, double *max_err, int *exact_mask) {
-    if (w < 2 || w > pif::kMaxFastW || !(beta > 0)) return pif::bad("w must be in [2, 8]");
+    if (w < 2 || w > pif::kMaxPolyW || !(beta > 0)) return pif::bad("w must be in [2, 14]");
     pif::EsPolyHost P;
     double e = 0.0;
     pif::build_es_poly(w, beta, &P, &e);

@@ -1118,6 +1118,336 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
 }
 
 // ----------------------------------------------------------------------------
+// wide windows (9 <= w <= 14): FMA "ring" kernels
+//
+// Same work items, chunks and cell order as the DMMA kernels, but the w x w
+// (a, b) pairs of the footprint are dealt to the 32 lanes (ceil(w^2/32) per
+// lane) and each lane keeps, per pair, a ring of w z-slots in registers
+// (slot s holds plane z == s mod w of the current cell's footprint).  Per
+// particle of a chunk, lane-owned pairs do acc[t][s] += (s wx[a] wy[b]) wz[s]:
+// w FMAs per pair, all lanes busy, no atomics until a plane leaves the ring.
+// The particle's z weights are stored rotated into slot order by the lane that
+// computes them, so the inner loop has compile-time register indices.
+// ----------------------------------------------------------------------------
+
+template <int W>
+struct RingStage {
+    double wx[kChunk][W + 1];   // [p][a] (spreading: times the strength)
+    double wy[kChunk][W + 1];   // [p][b]
+    double wz[kChunk][W + 1];   // [p][slot]: wz[c] at slot (k_p + c) mod W
+};
+
+// lane p: window weights of its particle into the stage (z rotated by its cell)
+template <int W>
+__device__ __forceinline__ void ring_weights(RingStage<W> &st, const double *tab, const EsPoly &P,
+                                             int lane, int cnt, double x, double y, double z,
+                                             double sc, double h, double rh, double beta, int n) {
+    if (lane < cnt) {
+        // one axis at a time: the ring accumulators stay live across this phase
+        double wt[W];
+        es_axis_weights<W>(axis_coord(x, h, rh), beta, P, tab, wt);
+#pragma unroll
+        for (int a = 0; a < W; ++a) st.wx[lane][a] = __dmul_rn(sc, wt[a]);
+        es_axis_weights<W>(axis_coord(y, h, rh), beta, P, tab, wt);
+#pragma unroll
+        for (int a = 0; a < W; ++a) st.wy[lane][a] = wt[a];
+        const double cz = axis_coord(z, h, rh);
+        es_axis_weights<W>(cz, beta, P, tab, wt);
+        const int r0 = pmod((int)stencil_start(cz, W), n) % W;
+#pragma unroll
+        for (int a = 0; a < W; ++a) {
+            const int sl = r0 + a >= W ? r0 + a - W : r0 + a;
+            st.wz[lane][sl] = wt[a];
+        }
+    }
+    __syncwarp();
+}
+
+// plane z (ring slot `slot`) leaves the ring: lane-owned pairs add their
+// value at (ix + a, iy + b, z) and clear the slot
+template <int W>
+__device__ __forceinline__ void ring_flush_slot(double (&acc)[(W * W + 31) / 32][W], int slot,
+                                                int lane, int ix, int iy, int n, int64_t z,
+                                                double *grid) {
+    constexpr int NP = (W * W + 31) / 32;
+#pragma unroll
+    for (int s = 0; s < W; ++s) {
+        if (s == slot) {
+#pragma unroll
+            for (int t = 0; t < NP; ++t) {
+                const int qq = lane + 32 * t;
+                const double v = acc[t][s];
+                if (qq < W * W && v != 0.0) {
+                    const int a = qq / W, b = qq - (qq / W) * W;
+                    const int xa = (ix + a) % n, yb = (iy + b) % n;   // w may exceed n
+                    atomicAdd(grid + ((int64_t)xa * n + yb) * n + z, v);
+                }
+                acc[t][s] = 0.0;
+            }
+        }
+    }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+spread_ring_kernel(const double *__restrict__ px, const double *__restrict__ py,
+                   const double *__restrict__ pz, const int64_t *__restrict__ pid,
+                   const int32_t *__restrict__ perm, const double *__restrict__ strengths, double q,
+                   const int32_t *__restrict__ cell_start, double *__restrict__ grid, int n,
+                   int seg, int nseg, double h, double beta, const EsPoly poly, unsigned int *work,
+                   const int2 *__restrict__ items, const int *__restrict__ n_items) {
+    constexpr int NP = (W * W + 31) / 32;
+    const int nitems = *n_items;
+    const double rh = __drcp_rn(h);
+    __shared__ RingStage<W> stage[kWarpsPerBlock];
+    __shared__ double tab[32];
+    if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    RingStage<W> &st = stage[threadIdx.x >> 5];
+    int pa[NP], pb[NP];
+#pragma unroll
+    for (int t = 0; t < NP; ++t) {
+        const int qq = lane + 32 * t;
+        pa[t] = qq < W * W ? qq / W : 0;
+        pb[t] = qq < W * W ? qq % W : 0;
+    }
+
+    for (;;) {
+        int item = 0;
+        if (lane == 0) item = (int)atomicAdd(work, 1u);
+        item = __shfl_sync(kFull, item, 0);
+        if (item >= nitems) break;
+        const int2 it = items[item];
+        const int col = it.x / nseg, sg = it.x - col * nseg;
+        const int ix = col / n, iy = col - ix * n;
+        const int k0 = sg * seg, k1 = min(k0 + seg, n);
+        const int base = col * n;
+        const int pbeg = cell_start[base + k0] + it.y * kItemParticles;
+        const int pend = min(pbeg + kItemParticles, cell_start[base + k1]);
+        double acc[NP][W];
+#pragma unroll
+        for (int t = 0; t < NP; ++t)
+#pragma unroll
+            for (int s = 0; s < W; ++s) acc[t][s] = 0.0;
+        int k = k0;
+        int cell_end = cell_start[base + k0 + 1];
+        while (cell_end <= pbeg) cell_end = cell_start[base + (++k) + 1];
+        int next_end = cell_start[base + min(k + 2, k1)];
+
+        double nx = 0.0, ny = 0.0, nz = 0.0, ns = q;
+        if (pbeg + lane < pend) {
+            const int i = perm ? perm[pbeg + lane] : pbeg + lane;
+            nx = px[i];
+            ny = py[i];
+            nz = pz[i];
+            if (strengths) ns = strengths[pid[i]];
+        }
+        for (int pos = pbeg; pos < pend; pos += kChunk) {
+            const int cnt = min(kChunk, pend - pos);
+            const double cx = nx, cy = ny, cz = nz, cs = ns;
+            if (pos + kChunk + lane < pend) {
+                const int i = perm ? perm[pos + kChunk + lane] : pos + kChunk + lane;
+                nx = px[i];
+                ny = py[i];
+                nz = pz[i];
+                if (strengths) ns = strengths[pid[i]];
+            }
+            ring_weights<W>(st, tab, poly, lane, cnt, cx, cy, cz, cs, h, rh, beta, n);
+            int j = 0;
+            while (j < cnt) {
+                if (pos + j >= cell_end) {   // plane k leaves the ring
+                    ring_flush_slot<W>(acc, k % W, lane, ix, iy, n, k % n, grid);
+                    ++k;
+                    cell_end = next_end;
+                    next_end = cell_start[base + min(k + 2, k1)];
+                    continue;
+                }
+                const int jend = min(cnt, cell_end - pos);
+                for (; j < jend; ++j) {
+                    double f[NP];
+#pragma unroll
+                    for (int t = 0; t < NP; ++t) f[t] = st.wx[j][pa[t]] * st.wy[j][pb[t]];
+#pragma unroll
+                    for (int s = 0; s < W; ++s) {
+                        const double zw = st.wz[j][s];
+#pragma unroll
+                        for (int t = 0; t < NP; ++t) acc[t][s] = fma(f[t], zw, acc[t][s]);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        for (; k < k1; ++k) ring_flush_slot<W>(acc, k % W, lane, ix, iy, n, k % n, grid);
+        // planes k1 .. k1 + W - 2 are still in the ring
+        for (int pl = k1; pl < k1 + W - 1; ++pl)
+            ring_flush_slot<W>(acc, pl % W, lane, ix, iy, n, pl % n, grid);
+    }
+}
+
+// Gather (+ push) for wide windows.  A warp walks its work item once per
+// field component d: the lane-owned (a, b) pairs hold a ring of w z-slots of
+// E_d in registers for the whole item (loaded for the first cell, one plane
+// swapped per cell step); per particle a lane forms
+// sum_t wx[a_t] wy[b_t] sum_s E_d[t][s] wz[s], the 32 lane partials are reduced
+// per particle through shared memory and E_d goes to a per-position scratch
+// (L2-resident).  A last walk pushes every particle exactly as
+// interp_mma_kernel does.  Window weights are recomputed per component walk.
+template <int W>
+struct RingGather {
+    double red[kChunk][kChunk + 1];   // [particle][lane] partial sums
+};
+
+template <int W>
+__device__ __forceinline__ void ring_load_plane(double (&g)[(W * W + 31) / 32][W], int slot,
+                                                const double4 *field, int comp, int lane, int ix,
+                                                int iy, int n, int64_t z) {
+    constexpr int NP = (W * W + 31) / 32;
+#pragma unroll
+    for (int s = 0; s < W; ++s) {
+        if (s == slot) {
+#pragma unroll
+            for (int t = 0; t < NP; ++t) {
+                const int qq = lane + 32 * t;
+                double v = 0.0;
+                if (qq < W * W) {
+                    const int a = qq / W, b = qq - (qq / W) * W;
+                    const double *f = reinterpret_cast<const double *>(
+                        field + ((int64_t)((ix + a) % n) * n + (iy + b) % n) * n + z);
+                    v = __ldg(f + comp);
+                }
+                g[t][s] = v;
+            }
+        }
+    }
+}
+
+template <int W, bool PUSH>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+interp_ring_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
+                   const int32_t *__restrict__ cell_start, const double4 *__restrict__ field,
+                   int seg, int nseg, double beta, const EsPoly poly, PushParams pp,
+                   int32_t *__restrict__ key, int32_t *__restrict__ rank,
+                   int32_t *__restrict__ count, double *__restrict__ partials,
+                   double *__restrict__ E_out, double *__restrict__ scratch, unsigned int *work,
+                   const int2 *__restrict__ items, const int *__restrict__ n_items) {
+    constexpr int NP = (W * W + 31) / 32;
+    const int nitems = *n_items;
+    extern __shared__ double4 ring_smem[];
+    RingStage<W> *stages = reinterpret_cast<RingStage<W> *>(ring_smem);
+    RingGather<W> *gathers = reinterpret_cast<RingGather<W> *>(stages + kWarpsPerBlock);
+    __shared__ double tab[32];
+    if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    RingStage<W> &st = stages[threadIdx.x >> 5];
+    RingGather<W> &rg = gathers[threadIdx.x >> 5];
+    const int n = pp.n;
+    const double h = pp.h;
+    const int64_t M = P.count;
+    int pa[NP], pb[NP];
+#pragma unroll
+    for (int t = 0; t < NP; ++t) {
+        const int qq = lane + 32 * t;
+        pa[t] = qq < W * W ? qq / W : 0;
+        pb[t] = qq < W * W ? qq % W : 0;
+    }
+    double dg[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+
+    for (;;) {
+        int item = 0;
+        if (lane == 0) item = (int)atomicAdd(work, 1u);
+        item = __shfl_sync(kFull, item, 0);
+        if (item >= nitems) break;
+        const int2 it = items[item];
+        const int col = it.x / nseg, sg = it.x - col * nseg;
+        const int ix = col / n, iy = col - ix * n;
+        const int k0 = sg * seg, k1 = min(k0 + seg, n);
+        const int base = col * n;
+        const int cb = cell_start[base + k0 + min(lane, k1 - k0)];   // seg <= 31
+        const int pbeg = __shfl_sync(kFull, cb, 0) + it.y * kItemParticles;
+        const int pend = min(pbeg + kItemParticles, __shfl_sync(kFull, cb, k1 - k0));
+        int kf = k0;
+        while (__shfl_sync(kFull, cb, kf - k0 + 1) <= pbeg) ++kf;
+
+#pragma unroll 1
+        for (int d = 0; d < 3; ++d) {
+            double g[NP][W];
+            int k = kf;
+#pragma unroll
+            for (int s = 0; s < W; ++s) {   // planes k .. k + W - 1 of the first cell
+                const int pl = k + ((s - k % W + W) % W);
+                ring_load_plane<W>(g, s, field, d, lane, ix, iy, n, pl % n);
+            }
+            int cell_end = __shfl_sync(kFull, cb, k - k0 + 1);
+            double nx = 0.0, ny = 0.0, nz = 0.0;
+            if (pbeg + lane < pend) {
+                const int i = perm ? perm[pbeg + lane] : pbeg + lane;
+                nx = P.x[i]; ny = P.y[i]; nz = P.z[i];
+            }
+            for (int pos = pbeg; pos < pend; pos += kChunk) {
+                const int cnt = min(kChunk, pend - pos);
+                const double x0 = nx, y0 = ny, z0 = nz;
+                if (pos + kChunk + lane < pend) {
+                    const int i = perm ? perm[pos + kChunk + lane] : pos + kChunk + lane;
+                    nx = P.x[i]; ny = P.y[i]; nz = P.z[i];
+                }
+                ring_weights<W>(st, tab, poly, lane, cnt, x0, y0, z0, 1.0, h, pp.rh, beta, n);
+                for (int j = 0; j < cnt; ++j) {
+                    while (pos + j >= cell_end) {   // next cell: plane k leaves, k + W enters
+                        ring_load_plane<W>(g, k % W, field, d, lane, ix, iy, n, (k + W) % n);
+                        ++k;
+                        cell_end = __shfl_sync(kFull, cb, k - k0 + 1);
+                    }
+                    double part = 0.0;
+#pragma unroll
+                    for (int t = 0; t < NP; ++t) {
+                        double inner = 0.0;
+#pragma unroll
+                        for (int s = 0; s < W; ++s) inner = fma(g[t][s], st.wz[j][s], inner);
+                        part = fma(st.wx[j][pa[t]] * st.wy[j][pb[t]], inner, part);
+                    }
+                    rg.red[j][lane] = part;
+                }
+                __syncwarp();
+                if (lane < cnt) {
+                    double e = 0.0;
+#pragma unroll 8
+                    for (int l = 0; l < 32; ++l) e += rg.red[lane][l];
+                    scratch[d * M + pos + lane] = e;
+                }
+                __syncwarp();
+            }
+        }
+        // push walk (the lane reads back its own scratch entries)
+        for (int pos = pbeg + lane; pos < pend; pos += 32) {
+            const int i = perm ? perm[pos] : pos;
+            const double E0 = scratch[pos], E1 = scratch[M + pos], E2 = scratch[2 * M + pos];
+            if (PUSH) {
+                double x = P.x[i], y = P.y[i], z = P.z[i];
+                double vx = P.vx[i], vy = P.vy[i], vz = P.vz[i];
+                const int64_t id = P.id[i];
+                boris_one(pp, E0, E1, E2, x, y, z, vx, vy, vz, dg);
+                Q.x[pos] = x; Q.y[pos] = y; Q.z[pos] = z;
+                Q.vx[pos] = vx; Q.vy[pos] = vy; Q.vz[pos] = vz;
+                Q.id[pos] = id;
+                mirror_store(pp, id, x, y, z, vx, vy, vz);
+                const int kk = cell_key(x, y, z, h, pp.rh, pp.w, n);
+                key[pos] = kk;
+                rank[pos] = atomicAdd(&count[kk], 1);
+            } else {
+                const int64_t o = 3 * P.id[i];
+                E_out[o] = E0;
+                E_out[o + 1] = E1;
+                E_out[o + 2] = E2;
+            }
+        }
+        __syncwarp();
+    }
+    if (PUSH) block_diag_store(dg, partials);
+}
+
+// ----------------------------------------------------------------------------
 // generic one-thread-per-particle kernels (any w <= kMaxW)
 // ----------------------------------------------------------------------------
 
@@ -1313,11 +1643,37 @@ int persistent_blocks(K kernel, int threads, size_t smem, int sm_count) {
     return per_sm * sm_count;
 }
 
+// Wide windows (9..14; 8 only when forced, for comparison) take the FMA ring
+// kernels: polynomial weights only, so the plan's polynomials must all be valid.
+// per-position E scratch of the ring gather (3 x M doubles), grown on demand
+int ensure_ring_scratch(Plan &p, int64_t M) {
+    if (3 * M <= p.ring_scratch_cap) return PIF_OK;
+    if (p.ring_scratch) cudaFree(p.ring_scratch);
+    p.ring_scratch = nullptr;
+    p.ring_scratch_cap = 0;
+    cudaError_t e = cudaMalloc(&p.ring_scratch, sizeof(double) * 3 * M);
+    if (e != cudaSuccess) return fail_cuda(e, "ring gather scratch");
+    p.ring_scratch_cap = 3 * M;
+    return PIF_OK;
+}
+
+// below ~2 particles per stencil cell the ring gather reloads a plane per
+// particle and the one-thread-per-particle gather is faster
+constexpr double kRingGatherMinDensity = 2.0;
+// the ring spreader flushes w^2 values per plane it passes: below ~1 particle
+// per cell the one-thread-per-particle atomics are cheaper
+constexpr double kRingSpreadMinDensity = 0.75;
+
+bool ring_path_ok(const Plan &p) {
+    if (p.force_generic || p.poly.exact_mask != 0) return false;
+    return (p.w >= 9 && p.w <= kMaxRingW) || (p.force_ring && p.w == 8);
+}
+
 // The DMMA kernels cover w <= 8; for w >= kPolyOnlyW they are compiled without
 // the exact-weight fallback, so a plan whose polynomials missed the bound there
 // (not the case for the reference's beta = 2.30 w) takes the generic kernels.
 bool fast_path_ok(const Plan &p) {
-    if (p.w > kMaxFastW || p.force_generic) return false;
+    if (p.w > kMaxFastW || p.force_generic || p.force_ring) return false;
     return p.w < kPolyOnlyW || p.poly.exact_mask == 0;
 }
 
@@ -1406,6 +1762,7 @@ int segment_cells(const Plan &p, int64_t M) {
 }
 
 int build_items(Plan &p, int64_t M, cudaStream_t s) {
+    p.density = (double)M / (double)p.n3;
     p.seg = segment_cells(p, M);
     p.n_segs = p.n * p.n * ((p.n + p.seg - 1) / p.seg);
     const int64_t need = p.n_segs + M / kItemParticles + 1;
@@ -1511,6 +1868,34 @@ int launch_spread(Plan &p, const pif_soa_t &P, const int32_t *perm, const double
                 return PIF_ERR_VALUE;
         }
 #undef PIF_SPREAD_CASE
+    } else if (ring_path_ok(p) && p.density >= kRingSpreadMinDensity) {
+        const int nseg = (p.n + p.seg - 1) / p.seg;
+        const int *nitems = p.seg_off + p.n_segs;
+        e = cudaMemsetAsync(p.work, 0, sizeof(unsigned int), s);
+        if (e != cudaSuccess) return fail_cuda(e, "zero work counter");
+        const int threads = kWarpsPerBlock * 32;
+#define PIF_RING_SPREAD_CASE(W)                                                              \
+    case W: {                                                                                \
+        auto k = spread_ring_kernel<W>;                                                     \
+        int blocks = persistent_blocks(k, threads, 0, p.sm_count);                           \
+        k<<<blocks, threads, 0, s>>>(P.x, P.y, P.z, P.id, perm, strengths, q, p.cell_start,   \
+                                     p.grid, p.n, p.seg, nseg, p.h, p.beta, poly, p.work,     \
+                                     p.items, nitems);                                       \
+        break;                                                                               \
+    }
+        switch (p.w) {
+            PIF_RING_SPREAD_CASE(8)
+            PIF_RING_SPREAD_CASE(9)
+            PIF_RING_SPREAD_CASE(10)
+            PIF_RING_SPREAD_CASE(11)
+            PIF_RING_SPREAD_CASE(12)
+            PIF_RING_SPREAD_CASE(13)
+            PIF_RING_SPREAD_CASE(14)
+            default:
+                set_error("unsupported window width");
+                return PIF_ERR_VALUE;
+        }
+#undef PIF_RING_SPREAD_CASE
     } else {
         spread_generic_kernel<<<grid_for(P.count, 128, p.sm_count), 128, 0, s>>>(
             P, strengths, q, p.grid, p.n, p.w, p.h, p.beta);
@@ -1584,6 +1969,38 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
                 return PIF_ERR_VALUE;
         }
 #undef PIF_INTERP_CASE
+    } else if (P.count > 0 && ring_path_ok(p) && p.density >= kRingGatherMinDensity) {
+        const int nseg = (p.n + p.seg - 1) / p.seg;
+        const int *nitems = p.seg_off + p.n_segs;
+        e = cudaMemsetAsync(p.work, 0, sizeof(unsigned int), s);
+        if (e != cudaSuccess) return fail_cuda(e, "zero work counter");
+        const int threads = kWarpsPerBlock * 32;
+#define PIF_RING_INTERP_CASE(W)                                                               \
+    case W: {                                                                                 \
+        const size_t dyn = kWarpsPerBlock * (sizeof(RingStage<W>) + sizeof(RingGather<W>));   \
+        if (ensure_ring_scratch(p, P.count) != PIF_OK) return PIF_ERR_CUDA;                    \
+        auto k = push ? interp_ring_kernel<W, true> : interp_ring_kernel<W, false>;           \
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);       \
+        blocks = persistent_blocks(k, threads, dyn, p.sm_count);                              \
+        if (blocks > p.partial_blocks) blocks = p.partial_blocks;                             \
+        k<<<blocks, threads, dyn, s>>>(P, perm, Q, p.cell_start, field, p.seg, nseg, p.beta,   \
+                                       poly, pp, key, rank, p.cell_count, p.partials, E_out,  \
+                                       p.ring_scratch, p.work, p.items, nitems);              \
+        break;                                                                                \
+    }
+        switch (p.w) {
+            PIF_RING_INTERP_CASE(8)
+            PIF_RING_INTERP_CASE(9)
+            PIF_RING_INTERP_CASE(10)
+            PIF_RING_INTERP_CASE(11)
+            PIF_RING_INTERP_CASE(12)
+            PIF_RING_INTERP_CASE(13)
+            PIF_RING_INTERP_CASE(14)
+            default:
+                set_error("unsupported window width");
+                return PIF_ERR_VALUE;
+        }
+#undef PIF_RING_INTERP_CASE
     } else {
         blocks = grid_for(P.count, 128, p.sm_count);
         if (blocks > p.partial_blocks) blocks = p.partial_blocks;

@@ -22,7 +22,9 @@ namespace pif {
 
 // Fused-kernel specialisations exist for stencil widths up to this value; wider
 // windows (eps < 1e-8) take the generic one-thread-per-particle path.
-constexpr int kMaxFastW = 8;
+constexpr int kMaxFastW = 8;    // DMMA kernels
+constexpr int kMaxPolyW = 14;   // polynomial weights: pair rows a <= 6 (EsPoly)
+constexpr int kMaxRingW = 14;   // FMA ring kernels (register ring of w slots per lane pair)
 constexpr int kMaxW = 17;          // eps >= 1e-16 (nufft.py:74)
 constexpr int kSub = 8;            // particles per warp sub-batch (fast kernels)
 constexpr int kWarpsPerBlock = 4;  // fast kernels: one work item per warp
@@ -43,6 +45,9 @@ struct Plan {
     int64_t n3 = 0, nhalf = 0;     // n^3, n*n*(n/2+1)
     int seg = 8;                   // cells per z-segment work item (set per binning)
     int seg_target = 512;          // particles per work item the segment length aims at
+    double density = 0.0;          // particles per stencil cell at the last binning
+    double *ring_scratch = nullptr;  // E per position for the wide-window gather
+    int64_t ring_scratch_cap = 0;
     double *mirror_x = nullptr;    // id-order (M,3) mirrors written by the push kernels
     double *mirror_v = nullptr;
     long long mirror_id0 = 0;
@@ -74,7 +79,8 @@ struct Plan {
     bool z2d_strided = false;      // Z2D writes the interleaved grid directly
     bool field_valid = false;
     bool interp_ws = false;         // warp-specialised gather+push (env PIF_INTERP_WS=1: on)
-    bool force_generic = false;     // env PIF_FORCE_GENERIC=1: one-thread-per-particle kernels
+    bool force_generic = false;
+    bool force_ring = false;       // PIF_FORCE_RING: w = 8 through the ring kernels (A/B)     // env PIF_FORCE_GENERIC=1: one-thread-per-particle kernels
     int sm_count = 148;
     int64_t bytes = 0;
     EsPolyHost poly{};              // interior weight polynomials for w <= 8

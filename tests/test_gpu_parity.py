@@ -597,3 +597,36 @@ def test_run_host_streaming_matches_pif_step(cuda):
     assert rel_max(xh.numpy(), st.ensemble.x) <= 1e-12
     assert rel_max(vh.numpy(), st.ensemble.v) <= 1e-12
     assert np.all(np.isfinite(wh.numpy())) and np.all(wh.numpy() > 0)
+
+
+@pytest.mark.parametrize("eps", [1e-9, 1e-12])
+def test_wide_window_ring_kernels_match_oracle(eps):
+    """w = 10 / 13 at ~5 particles per stencil cell: the FMA ring spreader and
+    gather (+ push via pif_step) against the oracle."""
+    o = oracle()
+    N, L, M = 8, 4 * np.pi, 20000
+    plan = pb.make_plan(N, L, eps)
+    op = o.make_plan(N, L, eps)
+    assert plan.window.w in (10, 13)
+    rng = np.random.default_rng(11)
+    x = rng.random((M, 3)) * L
+    v = rng.standard_normal((M, 3))
+    q = rng.standard_normal(M)
+    got = pb.type1(plan, x, q).coeffs
+    assert rel_l2(got, o.type1(op, x, q)) <= TIGHT
+    herm = [np.fft.fftshift(np.fft.fftn(rng.standard_normal((N,) * 3))) / 100 for _ in range(3)]
+    E = nufft.gather3_real(plan, herm, x)
+    assert rel_l2(E, o.gather3_real(op, herm, x)) <= TIGHT
+    # one full PIF step (deposit, Poisson, gather + Boris push) through the engine
+    spec = pb.landau_spec(N=N, ppm=1)
+    ens = pb.ParticleEnsemble(x=x.copy(), v=v.copy(), ids=np.arange(M), q_per_particle=-1.0 / M,
+                              m_per_particle=1.0 / M, total_charge=-1.0, total_mass=1.0,
+                              global_count=M)
+    st = pb.StepState(ensemble=ens, plan=plan, externals=spec.externals(), dt=0.05)
+    st = pb.pif_step(st)
+    rho = o.deposit_charge(x, -1.0 / M, op)
+    Eo = o.gather_efield(o.poisson_efield(rho, L), x, op)
+    xo, vo = o.boris_push(x.copy(), v.copy(), Eo, -1.0 / M, 1.0 / M, (0.0, 0.0, 0.0), "none",
+                          0.05, L)
+    assert rel_max(st.ensemble.v, vo) <= 1e-12
+    assert rel_max(st.ensemble.x, xo) <= 1e-12
