@@ -168,6 +168,16 @@ int pif_interp_perm(pif_plan_t plan, const pif_soa_t *parts, const int32_t *perm
  * id0 .. id0+M-1); v_out may be NULL. */
 int pif_soa_to_aos(pif_plan_t plan, const pif_soa_t *parts, int64_t id0, double *x_out,
                    double *v_out, void *stream);
+/* Spread -> gather weight cache.  The gather of a PD step runs at the positions
+ * the previous step's deposit spread (strategies.py:290-300: solve(x_n+1), then
+ * gather(x_n+1)), in the same perm order and chunking.  When enabled, the
+ * w <= 8 spread also stores its 3w window weights per particle (192 B each at
+ * w = 8, allocated on first use; if that fails the plan runs without) and the
+ * next gather over the same particle view and perm loads them instead of
+ * recomputing them.  Anything that moves or re-bins the particles invalidates
+ * the cache.  Default off; the Python engine enables it when HBM allows. */
+int pif_set_weight_cache(pif_plan_t plan, int enable);
+
 /* Host-layout (ParticleEnsemble, particles.py:10-62) streaming, used when the
  * caller keeps the particles in host memory between steps (pif_step,
  * pif.py:178-190):

@@ -54,7 +54,7 @@ int dalloc(Plan &p, T **ptr, size_t count) {
 void release(Plan &p) {
     void *ptrs[] = {p.deconv, p.kvec, p.grid, p.spec, p.field, p.field3, p.emodes, p.cgrid,
                     p.cell_count, p.cell_start, p.scan_tmp, p.work, p.partials, p.maxbits,
-                    p.shape_tab, p.items, p.seg_parts, p.seg_off, p.ring_scratch};
+                    p.shape_tab, p.items, p.seg_parts, p.seg_off, p.ring_scratch, p.wcache};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     if (p.d2z) cufftDestroy(p.d2z);
@@ -471,6 +471,19 @@ int pif_set_id_order_output(pif_plan_t plan, double *x_out, double *v_out, int64
     plan->p.mirror_x = x_out;
     plan->p.mirror_v = v_out;
     plan->p.mirror_id0 = id0;
+    return PIF_OK;
+}
+
+int pif_set_weight_cache(pif_plan_t plan, int enable) {
+    if (!plan) return pif::bad("null plan");
+    pif::Plan &p = plan->p;
+    p.wcache_on = enable != 0;
+    p.wcache_valid = false;
+    if (!p.wcache_on && p.wcache) {
+        cudaFree(p.wcache);
+        p.wcache = nullptr;
+        p.wcache_cap = 0;
+    }
     return PIF_OK;
 }
 

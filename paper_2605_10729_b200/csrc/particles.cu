@@ -213,7 +213,8 @@ template <int W, bool XYZ>
 __device__ __forceinline__ void chunk_weights(WarpChunk &st, const double *tab, const EsPoly &P,
                                               int lane, int cnt, double x, double y, double z,
                                               double s, bool scale, double h, double rh,
-                                              double beta) {
+                                              double beta, double *wc = nullptr,
+                                              int64_t wstride = 0, int64_t wpos = 0) {
     if (lane < cnt) {
         if (XYZ) {
             const double c[3] = {axis_coord(x, h, rh), axis_coord(y, h, rh), axis_coord(z, h, rh)};
@@ -226,19 +227,54 @@ __device__ __forceinline__ void chunk_weights(WarpChunk &st, const double *tab, 
                 st.wz[lane][a] = wt[2][a];
             }
         } else {
+            // wc: also keep the (unscaled) weights for the next gather at these
+            // positions, row 8 * axis + a of a [24][wstride] array, column wpos
             double wt[W];
             es_axis_weights<W>(axis_coord(x, h, rh), beta, P, tab, wt);
 #pragma unroll
-            for (int a = 0; a < W; ++a) st.wx[a][lane] = scale ? __dmul_rn(s, wt[a]) : wt[a];
+            for (int a = 0; a < W; ++a) {
+                st.wx[a][lane] = scale ? __dmul_rn(s, wt[a]) : wt[a];
+                if (wc) wc[a * wstride + wpos] = wt[a];
+            }
             es_axis_weights<W>(axis_coord(y, h, rh), beta, P, tab, wt);
 #pragma unroll
-            for (int a = 0; a < W; ++a) st.wy[lane][a] = wt[a];
+            for (int a = 0; a < W; ++a) {
+                st.wy[lane][a] = wt[a];
+                if (wc) wc[(8 + a) * wstride + wpos] = wt[a];
+            }
             es_axis_weights<W>(axis_coord(z, h, rh), beta, P, tab, wt);
 #pragma unroll
-            for (int a = 0; a < W; ++a) st.wz[lane][a] = wt[a];
+            for (int a = 0; a < W; ++a) {
+                st.wz[lane][a] = wt[a];
+                if (wc) wc[(16 + a) * wstride + wpos] = wt[a];
+            }
         }
     }
     __syncwarp();
+}
+
+// The gather's window weights from the cache the preceding spread wrote
+// (same particles, same perm, same chunking): lane l copies its particle's
+// 3 x w weights into the stage with cp.async (one commit group per chunk).
+template <int W>
+__device__ __forceinline__ void chunk_weights_async(WarpChunk &st, const double *wc,
+                                                    int64_t wstride, int64_t wpos, int lane,
+                                                    int cnt) {
+    if (lane < cnt) {
+#pragma unroll
+        for (int a = 0; a < W; ++a) {
+            const unsigned dx = (unsigned)__cvta_generic_to_shared(&st.wx[a][lane]);
+            const unsigned dy = (unsigned)__cvta_generic_to_shared(&st.wy[lane][a]);
+            const unsigned dz = (unsigned)__cvta_generic_to_shared(&st.wz[lane][a]);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dx),
+                         "l"(wc + a * wstride + wpos));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dy),
+                         "l"(wc + (8 + a) * wstride + wpos));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dz),
+                         "l"(wc + (16 + a) * wstride + wpos));
+        }
+    }
+    asm volatile("cp.async.commit_group;");
 }
 
 // ----------------------------------------------------------------------------
@@ -290,7 +326,8 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
                   const int32_t *__restrict__ perm, const double *__restrict__ strengths, double q,
                   const int32_t *__restrict__ cell_start, double *__restrict__ grid, int n,
                   int seg, int nseg, double h, double beta, const EsPoly poly, unsigned int *work,
-                  const int2 *__restrict__ items, const int *__restrict__ n_items) {
+                  const int2 *__restrict__ items, const int *__restrict__ n_items,
+                  double *__restrict__ wc, int64_t wstride) {
     const int nitems = *n_items;
     const double rh = __drcp_rn(h);
     __shared__ WarpChunk stage[kWarpsPerBlock];
@@ -343,7 +380,8 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
                 nz = pz[i];
                 if (strengths) ns = strengths[pid[i]];
             }
-            chunk_weights<W, false>(st, tab, poly, lane, cnt, cx, cy, cz, cs, true, h, rh, beta);
+            chunk_weights<W, false>(st, tab, poly, lane, cnt, cx, cy, cz, cs, true, h, rh, beta, wc,
+                                    wstride, pos + lane);
             int j = 0;
             while (j < cnt) {
                 if (pos + j >= cell_end) {
@@ -959,21 +997,32 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                   const EsPoly poly, PushParams pp, int32_t *__restrict__ key,
                   int32_t *__restrict__ rank, int32_t *__restrict__ count,
                   double *__restrict__ partials, double *__restrict__ E_out, unsigned int *work,
-                  const int2 *__restrict__ items, const int *__restrict__ n_items) {
+                  const int2 *__restrict__ items, const int *__restrict__ n_items,
+                  const double *__restrict__ wc, int64_t wstride) {
     const int nitems = *n_items;
     __shared__ WarpChunk stage[kWarpsPerBlock];
     __shared__ double4 planes[kWarpsPerBlock][8][8];
     __shared__ double tab[32];
-#if PIF_GATHER_DEFER
     extern __shared__ double4 dyn_smem[];
+#if PIF_GATHER_DEFER
     GatherPartials &gpart = reinterpret_cast<GatherPartials *>(dyn_smem)[threadIdx.x >> 5];
+    WarpChunk *stage2 = reinterpret_cast<WarpChunk *>(
+        reinterpret_cast<GatherPartials *>(dyn_smem) + kWarpsPerBlock);
+#else
+    WarpChunk *stage2 = reinterpret_cast<WarpChunk *>(dyn_smem);
 #endif
     if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    WarpChunk &st = stage[threadIdx.x >> 5];
+    WarpChunk &st0 = stage[threadIdx.x >> 5];
+    // with the weight cache, chunks alternate between two stages (the next
+    // chunk's weights land by cp.async while this one is gathered)
+    WarpChunk &st1 = wc ? stage2[threadIdx.x >> 5] : st0;
     double4 (*pf)[8] = planes[threadIdx.x >> 5];
-    chunk_zero(st, lane);
+    chunk_zero(st0, lane);
+    if (wc) chunk_zero(st1, lane);
+    int wb = 0;            // stage of the current chunk
+    bool wnewest = false;  // the newest cp.async group holds weights (not a plane)
     const int n = pp.n;
     const double h = pp.h;
     const int r = lane >> 2, c4 = lane & 3;
@@ -1022,7 +1071,12 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
         int k = kf;
         int cell_end = __shfl_sync(kFull, cb, kf - k0 + 1);
         prefetch_wait();   // previous item's outstanding prefetch
+        if (wc) {          // first chunk's cached weights
+            chunk_weights_async<W>(wb ? st1 : st0, wc, wstride, pbeg + lane, lane,
+                                   min(kChunk, pend - pbeg));
+        }
         prefetch_plane(pf, field, ix, iy, n, (kf + 8) % n, lane);
+        wnewest = false;
 
         for (int pos = pbeg; pos < pend; pos += kChunk) {
             const int cnt = min(kChunk, pend - pos);
@@ -1039,7 +1093,22 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                 if (perm || !PUSH || pp.mx) nid = P.id[i];
             }
             PHASE_MARK(t0);
-            chunk_weights<W, true>(st, tab, poly, lane, cnt, x0, y0, z0, 1.0, false, h, pp.rh, beta);
+            WarpChunk &st = wb ? st1 : st0;
+            if (wc) {
+                if (pos + kChunk < pend) {   // next chunk's weights into the other stage
+                    chunk_weights_async<W>(wb ? st0 : st1, wc, wstride, pos + kChunk + lane,
+                                           lane, min(kChunk, pend - pos - kChunk));
+                    asm volatile("cp.async.wait_group 1;" ::: "memory");
+                    wnewest = true;
+                } else {
+                    asm volatile("cp.async.wait_group 0;" ::: "memory");
+                    wnewest = false;
+                }
+                __syncwarp();
+            } else {
+                chunk_weights<W, true>(st, tab, poly, lane, cnt, x0, y0, z0, 1.0, false, h, pp.rh,
+                                       beta);
+            }
             PHASE_MARK(t1);
             PHASE_ADD(0, t0, t1);
             int j = 0;
@@ -1047,7 +1116,12 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                 const int gp = pos + j;
                 if (gp >= cell_end) {   // next cell: plane k leaves slot k&7, plane k+8 enters
                     const int s = k & 7;
-                    prefetch_wait();
+                    if (wnewest) {   // the plane group is older than the weights group
+                        asm volatile("cp.async.wait_group 1;" ::: "memory");
+                        __syncwarp();
+                    } else {
+                        prefetch_wait();
+                    }
                     if (c4 == (s & 3)) {
                         if (s >> 2) plane_from_smem(g, 1, pf, r);
                         else plane_from_smem(g, 0, pf, r);
@@ -1055,6 +1129,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                     __syncwarp();
                     ++k;
                     prefetch_plane(pf, field, ix, iy, n, (k + 8) % n, lane);
+                    wnewest = false;
                     cell_end = __shfl_sync(kFull, cb, k - k0 + 1);
                     continue;
                 }
@@ -1106,6 +1181,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
             ph[3] += 1;
             ph[4] += (unsigned long long)cnt;
 #endif
+            if (wc) wb ^= 1;
         }
     }
 #ifdef PIF_PHASE_TIMING
@@ -1711,6 +1787,7 @@ PushParams make_push(const Plan &p, double half, double dt, const double *tq, co
 // ============================================================================
 
 int launch_wrap(Plan &p, double *x, double *y, double *z, int64_t M, cudaStream_t s) {
+    p.wcache_valid = false;
     if (M == 0) return PIF_OK;
     wrap_kernel<<<grid_for(M, 256, p.sm_count), 256, 0, s>>>(x, y, z, M, p.L);
     return fail_cuda(cudaGetLastError(), "wrap_kernel");
@@ -1725,6 +1802,7 @@ int launch_bin_keys(Plan &p, const pif_soa_t &src, int32_t *key, int32_t *rank, 
 
 int launch_bin_scatter(Plan &p, const pif_soa_t &src, pif_soa_t &dst, const int32_t *key,
                        const int32_t *rank, bool vel, cudaStream_t s) {
+    p.wcache_valid = false;
     size_t tmp = p.scan_tmp_bytes;
     cudaError_t e = cub::DeviceScan::ExclusiveSum(p.scan_tmp, tmp, p.cell_count, p.cell_start,
                                                   (int)(p.n3 + 1), s);
@@ -1809,6 +1887,7 @@ int debug_phase_cycles(unsigned long long *out) {
 
 int launch_load_aos(Plan &p, const double *x, const double *v, int64_t id0, pif_soa_t &dst,
                     int32_t *key, int32_t *rank, cudaStream_t s) {
+    p.wcache_valid = false;
     if (dst.count == 0) return PIF_OK;
     load_aos_kernel<<<grid_for(dst.count, 256, p.sm_count), 256, 0, s>>>(
         x, v, id0, dst.count, dst, p.L, p.h, p.w, p.n, key, rank, p.cell_count);
@@ -1817,6 +1896,7 @@ int launch_load_aos(Plan &p, const double *x, const double *v, int64_t id0, pif_
 
 int launch_bin_perm(Plan &p, const int32_t *key, const int32_t *rank, int64_t M, int32_t *perm,
                     cudaStream_t s) {
+    p.wcache_valid = false;
     size_t tmp = p.scan_tmp_bytes;
     cudaError_t e = cub::DeviceScan::ExclusiveSum(p.scan_tmp, tmp, p.cell_count, p.cell_start,
                                                   (int)(p.n3 + 1), s);
@@ -1839,12 +1919,21 @@ int launch_spread(Plan &p, const pif_soa_t &P, const int32_t *perm, const double
     cudaError_t e = cudaMemsetAsync(p.grid, 0, sizeof(double) * p.n3, s);
     if (e != cudaSuccess) return fail_cuda(e, "zero grid");
     if (P.count == 0) return PIF_OK;
+    p.wcache_valid = false;
     if (fast_path_ok(p)) {
         const int nseg = (p.n + p.seg - 1) / p.seg;
         const int *nitems = p.seg_off + p.n_segs;
         e = cudaMemsetAsync(p.work, 0, sizeof(unsigned int), s);
         if (e != cudaSuccess) return fail_cuda(e, "zero work counter");
         const int threads = kWarpsPerBlock * 32;
+        // keep this spread's window weights for the gather at the same positions
+        double *wc = (p.wcache_on && ensure_wcache(p, P.count) == PIF_OK) ? p.wcache : nullptr;
+        if (wc) {
+            p.wcache_valid = true;
+            p.wcache_x = P.x;
+            p.wcache_perm = perm;
+            p.wcache_count = P.count;
+        }
 #define PIF_SPREAD_CASE(W)                                                                   \
     case W: {                                                                                \
         auto k = spread_mma_kernel<W>;                                                      \
@@ -1852,7 +1941,7 @@ int launch_spread(Plan &p, const pif_soa_t &P, const int32_t *perm, const double
         k<<<blocks, threads, 0, s>>>(P.x, P.y, P.z, P.id, perm, strengths, q, p.cell_start,   \
                                      p.grid,                                                 \
                                      p.n, p.seg, nseg, p.h, p.beta, poly, p.work, p.items,   \
-                                     nitems);                                                \
+                                     nitems, wc, P.count);                                   \
         break;                                                                               \
     }
         switch (p.w) {
@@ -1903,8 +1992,26 @@ int launch_spread(Plan &p, const pif_soa_t &P, const int32_t *perm, const double
     return fail_cuda(cudaGetLastError(), "spread kernel");
 }
 
-// dynamic shared memory of interp_mma_kernel: the per-warp partial sums
+// dynamic shared memory of interp_mma_kernel: the per-warp partial sums (+ the
+// second weight stage when the weight cache is in use)
 constexpr int kGatherDyn = PIF_GATHER_DEFER ? (int)(kWarpsPerBlock * sizeof(GatherPartials)) : 0;
+constexpr int kGatherDynMax = kGatherDyn + (int)(kWarpsPerBlock * sizeof(WarpChunk));
+
+// spread -> gather window-weight cache, [24][M] doubles, grown on demand
+int ensure_wcache(Plan &p, int64_t M) {
+    if (24 * M <= p.wcache_cap) return PIF_OK;
+    if (p.wcache) cudaFree(p.wcache);
+    p.wcache = nullptr;
+    p.wcache_cap = 0;
+    cudaError_t e = cudaMalloc(&p.wcache, sizeof(double) * 24 * M);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        p.wcache_on = false;   // no room: run without the cache
+        return PIF_ERR_CUDA;
+    }
+    p.wcache_cap = 24 * M;
+    return PIF_OK;
+}
 
 int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q, bool push,
                   double half, double dt, const double *tq, const double *sq, int has_b,
@@ -1925,6 +2032,12 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
         e = cudaMemsetAsync(p.work, 0, sizeof(unsigned int), s);
         if (e != cudaSuccess) return fail_cuda(e, "zero work counter");
         const int threads = kWarpsPerBlock * 32;
+        // weights cached by the spread at exactly these particles / this order
+        const double *wc = (p.wcache_on && p.wcache_valid && p.wcache_x == P.x &&
+                            p.wcache_perm == perm && p.wcache_count == P.count)
+                               ? p.wcache
+                               : nullptr;
+        const size_t dyn = kGatherDyn + (wc ? kWarpsPerBlock * sizeof(WarpChunk) : 0);
 #define PIF_INTERP_CASE(W)                                                                    \
     case W: {                                                                                 \
         if (push && p.interp_ws && !pp.mx) {                                                  \
@@ -1936,23 +2049,23 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
                                     nitems);                                                  \
         } else if (push) {                                                                    \
             auto k = interp_mma_kernel<W, true>;                                             \
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kGatherDyn);  \
-            blocks = persistent_blocks(k, threads, kGatherDyn, p.sm_count);                   \
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kGatherDynMax); \
+            blocks = persistent_blocks(k, threads, dyn, p.sm_count);                          \
             if (blocks > p.partial_blocks) blocks = p.partial_blocks;                         \
-            k<<<blocks, threads, kGatherDyn, s>>>(P, perm, Q, p.cell_start, field, p.seg, nseg,  \
+            k<<<blocks, threads, dyn, s>>>(P, perm, Q, p.cell_start, field, p.seg, nseg,      \
                                                   p.beta,                                     \
                                          poly, pp,                                            \
                                          key, rank, p.cell_count, p.partials, E_out, p.work,   \
-                                         p.items, nitems);                                    \
+                                         p.items, nitems, wc, P.count);                       \
         } else {                                                                              \
             auto k = interp_mma_kernel<W, false>;                                            \
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kGatherDyn);  \
-            blocks = persistent_blocks(k, threads, kGatherDyn, p.sm_count);                   \
-            k<<<blocks, threads, kGatherDyn, s>>>(P, perm, Q, p.cell_start, field, p.seg, nseg,  \
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kGatherDynMax); \
+            blocks = persistent_blocks(k, threads, dyn, p.sm_count);                          \
+            k<<<blocks, threads, dyn, s>>>(P, perm, Q, p.cell_start, field, p.seg, nseg,      \
                                                   p.beta,                                     \
                                          poly, pp,                                            \
                                          key, rank, p.cell_count, p.partials, E_out, p.work,   \
-                                         p.items, nitems);                                    \
+                                         p.items, nitems, wc, P.count);                       \
         }                                                                                     \
         break;                                                                                \
     }
@@ -2010,6 +2123,7 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) return fail_cuda(e, "interp kernel");
+    if (push) p.wcache_valid = false;   // the particles moved
     if (push) {
         if (P.count == 0) {
             e = cudaMemsetAsync(diag, 0, sizeof(double) * kDiagSlots, s);

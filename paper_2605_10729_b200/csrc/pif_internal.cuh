@@ -47,6 +47,13 @@ struct Plan {
     int seg_target = 512;          // particles per work item the segment length aims at
     double density = 0.0;          // particles per stencil cell at the last binning
     double *ring_scratch = nullptr;  // E per position for the wide-window gather
+    bool wcache_on = false;        // spread keeps its window weights for the next gather
+    double *wcache = nullptr;
+    int64_t wcache_cap = 0;
+    bool wcache_valid = false;     // wcache matches (wcache_x, wcache_perm, wcache_count)
+    const double *wcache_x = nullptr;
+    const int32_t *wcache_perm = nullptr;
+    int64_t wcache_count = 0;
     int64_t ring_scratch_cap = 0;
     double *mirror_x = nullptr;    // id-order (M,3) mirrors written by the push kernels
     double *mirror_v = nullptr;
@@ -104,6 +111,7 @@ int launch_bin_perm(Plan &p, const int32_t *key, const int32_t *rank, int64_t M,
                     cudaStream_t s);
 int launch_spread(Plan &p, const pif_soa_t &parts, const int32_t *perm, const double *strengths,
                   double q, cudaStream_t s);
+int ensure_wcache(Plan &p, int64_t M);
 int launch_load_aos(Plan &p, const double *x, const double *v, int64_t id0, pif_soa_t &dst,
                     int32_t *key, int32_t *rank, cudaStream_t s);
 int launch_interp(Plan &p, const pif_soa_t &src, const int32_t *perm, pif_soa_t &dst, bool push,

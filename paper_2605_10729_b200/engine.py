@@ -76,6 +76,22 @@ class PifEngine:
         self.rec = None
         self.dtimers = DeviceTimers(enabled=False)
         self.launches = 0   # native kernel launches issued (for bench accounting)
+        self.weight_cache = self._enable_weight_cache()
+
+    def _enable_weight_cache(self) -> bool:
+        """PIF_WEIGHT_CACHE=1: the spread keeps its window weights for the next
+        gather (192 B per particle at w = 8, if HBM has room).  Off by default:
+        on B200 it trades 2 x 25.8 GB of HBM traffic per step at 2^27 particles
+        for the gather's weight evaluation, a net ~2%."""
+        import os
+        torch = require_cuda()
+        want = os.environ.get("PIF_WEIGHT_CACHE", "0").strip() not in ("0", "", "false", "off")
+        on = False
+        if want and self.plan.window.w <= 8:
+            free, _ = torch.cuda.mem_get_info(self.device)
+            on = free > 24 * 8 * self.count + (4 << 30)
+        _native.call("pif_set_weight_cache", self.handle, 1 if on else 0)
+        return on
 
     # -- plumbing -------------------------------------------------------------
     def _stream(self):

@@ -630,3 +630,27 @@ def test_wide_window_ring_kernels_match_oracle(eps):
                           0.05, L)
     assert rel_max(st.ensemble.v, vo) <= 1e-12
     assert rel_max(st.ensemble.x, xo) <= 1e-12
+
+
+def test_weight_cache_matches_recomputed_weights(cuda, monkeypatch):
+    """PIF_WEIGHT_CACHE=1 (spread keeps its weights, the next gather loads
+    them) steps identically, eager and from a CUDA graph, to the default."""
+    import torch
+
+    from paper_2605_10729_b200.engine import PifEngine
+    spec = pb.landau_spec(N=16, ppm=64, dt=0.05, seed=1)
+    M = spec.num_particles
+    plan = pb.make_plan(spec.N, spec.L, 1e-7)
+    ens = pb.sample_landau(spec, 1)
+    tables = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("PIF_WEIGHT_CACHE", flag)
+        eng = PifEngine(plan, M, "cuda", q=ens.q_per_particle, m=ens.m_per_particle,
+                        externals=spec.externals(), dt=spec.dt)
+        assert eng.weight_cache == (flag == "1")
+        eng.load(ens.x, ens.v, ens.ids)
+        tables.append(eng.run(12, graph=True).cpu().numpy())
+        x, v = eng.to_id_order()
+        tables.append(torch.cat([x, v], 1).cpu().numpy())
+    assert rel_max(tables[2][:, :6], tables[0][:, :6]) <= 1e-12
+    assert rel_max(tables[3], tables[1]) <= 1e-12
