@@ -34,6 +34,11 @@ class RunSetup:
     eps: float = 1e-7
     shape: str = "delta"
     diag_every: int = 1
+    # "host": the reference's numpy sampler (bit-identical ensembles);
+    # "device": the same streams regenerated in HBM (pif_sample_*, equal to
+    # libm ulps); "auto": device above 2^22 particles, where the reference's
+    # per-rank materialisation of the global ensemble stops fitting host memory
+    sampler: str = "auto"
 
 
 @dataclass(frozen=True)
@@ -86,13 +91,21 @@ def _run_replicated(setup: RunSetup, comm: Comm | None, timers: Timers, device=N
     size = comm.size if comm is not None else 1
     rank = comm.rank if comm is not None else 0
     lo, hi = id_slice(spec.num_particles, rank, size)
-    ens = sample_benchmark(spec, spec.seed, (lo, hi))
+    n_p = spec.num_particles
+    q, m = spec.Q_e / n_p, abs(spec.Q_e) / n_p        # bench.py:194-201
+    if setup.sampler not in ("auto", "host", "device"):
+        raise ValueError(f"unknown sampler {setup.sampler!r}")
+    on_device = setup.sampler == "device" or (setup.sampler == "auto" and n_p > (1 << 22))
     dev = torch.device(device) if device is not None else torch.device(
         "cuda", torch.cuda.current_device())
     with torch.cuda.device(dev):
-        eng = PifEngine(plan, ens.count, dev, q=ens.q_per_particle, m=ens.m_per_particle,
-                        externals=externals, dt=spec.dt, shape=setup.shape, comm=comm)
-        eng.load(ens.x, ens.v, ens.ids)
+        eng = PifEngine(plan, hi - lo, dev, q=q, m=m, externals=externals, dt=spec.dt,
+                        shape=setup.shape, comm=comm)
+        if on_device:
+            eng.load_sampled(spec, (lo, hi))
+        else:
+            ens = sample_benchmark(spec, spec.seed, (lo, hi))
+            eng.load(ens.x, ens.v, ens.ids)
         torch.cuda.synchronize(dev)
         start = _time.perf_counter()
         table = eng.run(spec.steps, timers=timers)
@@ -103,9 +116,8 @@ def _run_replicated(setup: RunSetup, comm: Comm | None, timers: Timers, device=N
         from .pif import FieldSymmetryError
         raise FieldSymmetryError(f"field modes lost Hermitian symmetry (relative mismatch "
                                  f"{guard:.3e})")
-    recs = records_from_table(host, steps=spec.steps, dt=spec.dt, q=ens.q_per_particle,
-                              m=ens.m_per_particle, total_charge=spec.Q_e,
-                              diag_every=setup.diag_every)
+    recs = records_from_table(host, steps=spec.steps, dt=spec.dt, q=q, m=m,
+                              total_charge=spec.Q_e, diag_every=setup.diag_every)
     initial, records = recs[0], recs[1:]
     # the reference's Recorder stamps t = (i+1)*dt for step i+1 (strategies.py:301)
     for r in records:

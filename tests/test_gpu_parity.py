@@ -654,3 +654,14 @@ def test_weight_cache_matches_recomputed_weights(cuda, monkeypatch):
         tables.append(torch.cat([x, v], 1).cpu().numpy())
     assert rel_max(tables[2][:, :6], tables[0][:, :6]) <= 1e-12
     assert rel_max(tables[3], tables[1]) <= 1e-12
+
+
+def test_pd_run_with_device_sampler_matches_reference_trace():
+    """RunSetup(sampler="device"): ranks regenerate their slices of the reference
+    ensemble in HBM; the 20-step trace still matches the reference's PD-2 trace."""
+    spec, _ = _config1("landau")
+    setup = pb.RunSetup(spec=spec, eps=1e-7, sampler="device")
+    res = pb.spawn_spmd(2, lambda ctx: pb.run_particle_decomposition(setup, ctx))
+    got, ref = _trace(res[0]), CFG["landau_pd2_trace"]
+    for col in (2, 3, 4):
+        assert np.max(np.abs(got[:, col] - ref[:, col]) / np.abs(ref[:, col])) <= 1e-9
