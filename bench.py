@@ -390,8 +390,9 @@ def run_e2e(a, eng, torch, dist, world, per_gpu, glob, dev):
     return {"value": glob * K / T, "unit": UNIT, "h2d_bytes_per_step": M * 48 * world,
             "d2h_bytes_per_step": (M * 48 + 8) * world, "steps": K,
             "api": "PifEngine.run_host (pif_step-style): per step H2D x,v (pinned, id order) -> "
-                   "load/bin -> deposit -> allreduce -> solve_fields -> gather_push -> id-order "
-                   "scatter -> D2H x,v,W; step s's D2H and step s+1's H2D chunk-pipelined"}
+                   "fused AoS load/wrap/keys + bin -> deposit -> allreduce -> solve_fields -> "
+                   "gather+push (also writing x,v in id order) -> D2H x,v,W; step s's D2H and "
+                   "step s+1's H2D chunk-pipelined"}
 
 
 def main():
