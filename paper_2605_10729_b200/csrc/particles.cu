@@ -989,8 +989,13 @@ interp_ws_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
 #define PIF_GATHER_DEFER 1
 #endif
 
+#ifndef PIF_GATHER_WARPS
+#define PIF_GATHER_WARPS 4
+#endif
+constexpr int kGatherWarps = PIF_GATHER_WARPS;   // warps per gather block
+
 template <int W, bool PUSH>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, PIF_INTERP_MINB)
+__global__ void __launch_bounds__(kGatherWarps * 32, PIF_INTERP_MINB)
 interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                   const int32_t *__restrict__ cell_start,
                   const double4 *__restrict__ field, int seg, int nseg, double beta,
@@ -1000,14 +1005,14 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                   const int2 *__restrict__ items, const int *__restrict__ n_items,
                   const double *__restrict__ wc, int64_t wstride) {
     const int nitems = *n_items;
-    __shared__ WarpChunk stage[kWarpsPerBlock];
+    __shared__ WarpChunk stage[kGatherWarps];
     __shared__ double4 planes[kWarpsPerBlock][8][8];
     __shared__ double tab[32];
     extern __shared__ double4 dyn_smem[];
 #if PIF_GATHER_DEFER
     GatherPartials &gpart = reinterpret_cast<GatherPartials *>(dyn_smem)[threadIdx.x >> 5];
     WarpChunk *stage2 = reinterpret_cast<WarpChunk *>(
-        reinterpret_cast<GatherPartials *>(dyn_smem) + kWarpsPerBlock);
+        reinterpret_cast<GatherPartials *>(dyn_smem) + kGatherWarps);
 #else
     WarpChunk *stage2 = reinterpret_cast<WarpChunk *>(dyn_smem);
 #endif
@@ -1994,8 +1999,8 @@ int launch_spread(Plan &p, const pif_soa_t &P, const int32_t *perm, const double
 
 // dynamic shared memory of interp_mma_kernel: the per-warp partial sums (+ the
 // second weight stage when the weight cache is in use)
-constexpr int kGatherDyn = PIF_GATHER_DEFER ? (int)(kWarpsPerBlock * sizeof(GatherPartials)) : 0;
-constexpr int kGatherDynMax = kGatherDyn + (int)(kWarpsPerBlock * sizeof(WarpChunk));
+constexpr int kGatherDyn = PIF_GATHER_DEFER ? (int)(kGatherWarps * sizeof(GatherPartials)) : 0;
+constexpr int kGatherDynMax = kGatherDyn + (int)(kGatherWarps * sizeof(WarpChunk));
 
 // spread -> gather window-weight cache, [24][M] doubles, grown on demand
 int ensure_wcache(Plan &p, int64_t M) {
@@ -2037,7 +2042,8 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
                             p.wcache_perm == perm && p.wcache_count == P.count)
                                ? p.wcache
                                : nullptr;
-        const size_t dyn = kGatherDyn + (wc ? kWarpsPerBlock * sizeof(WarpChunk) : 0);
+        const size_t dyn = kGatherDyn + (wc ? kGatherWarps * sizeof(WarpChunk) : 0);
+        const int gthreads = kGatherWarps * 32;
 #define PIF_INTERP_CASE(W)                                                                    \
     case W: {                                                                                 \
         if (push && p.interp_ws && !pp.mx) {                                                  \
@@ -2050,9 +2056,9 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
         } else if (push) {                                                                    \
             auto k = interp_mma_kernel<W, true>;                                             \
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kGatherDynMax); \
-            blocks = persistent_blocks(k, threads, dyn, p.sm_count);                          \
+            blocks = persistent_blocks(k, gthreads, dyn, p.sm_count);                         \
             if (blocks > p.partial_blocks) blocks = p.partial_blocks;                         \
-            k<<<blocks, threads, dyn, s>>>(P, perm, Q, p.cell_start, field, p.seg, nseg,      \
+            k<<<blocks, gthreads, dyn, s>>>(P, perm, Q, p.cell_start, field, p.seg, nseg,     \
                                                   p.beta,                                     \
                                          poly, pp,                                            \
                                          key, rank, p.cell_count, p.partials, E_out, p.work,   \
@@ -2060,8 +2066,8 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
         } else {                                                                              \
             auto k = interp_mma_kernel<W, false>;                                            \
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kGatherDynMax); \
-            blocks = persistent_blocks(k, threads, dyn, p.sm_count);                          \
-            k<<<blocks, threads, dyn, s>>>(P, perm, Q, p.cell_start, field, p.seg, nseg,      \
+            blocks = persistent_blocks(k, gthreads, dyn, p.sm_count);                         \
+            k<<<blocks, gthreads, dyn, s>>>(P, perm, Q, p.cell_start, field, p.seg, nseg,     \
                                                   p.beta,                                     \
                                          poly, pp,                                            \
                                          key, rank, p.cell_count, p.partials, E_out, p.work,   \
