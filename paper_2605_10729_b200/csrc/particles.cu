@@ -2036,7 +2036,6 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
         const int *nitems = p.seg_off + p.n_segs;
         e = cudaMemsetAsync(p.work, 0, sizeof(unsigned int), s);
         if (e != cudaSuccess) return fail_cuda(e, "zero work counter");
-        const int threads = kWarpsPerBlock * 32;
         // weights cached by the spread at exactly these particles / this order
         const double *wc = (p.wcache_on && p.wcache_valid && p.wcache_x == P.x &&
                             p.wcache_perm == perm && p.wcache_count == P.count)
