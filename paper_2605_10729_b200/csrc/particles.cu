@@ -296,12 +296,15 @@ __device__ __forceinline__ void spread_flush_plane(double (&acc)[8][2], int k, i
     const int s = k & 7;
     if (c4 == (s >> 1)) {
         const int j = s & 1;
-        const int z = k % n;
+        const int z = k;   // cells of an item never wrap: k < n
+        const int64_t nn = (int64_t)n * n;
+        int64_t off = ((int64_t)ix * n + yrow) * n + z;
 #pragma unroll
         for (int a = 0; a < W; ++a) {
             const double v = j ? acc[a][1] : acc[a][0];
-            PIF_CHECK(((int64_t)((ix + a) % n) * n + yrow) * n + z < (int64_t)n * n * n);
-            if (v != 0.0) atomicAdd(grid + ((int64_t)((ix + a) % n) * n + yrow) * n + z, v);
+            PIF_CHECK(off == ((int64_t)((ix + a) % n) * n + yrow) * n + z);
+            if (v != 0.0) atomicAdd(grid + off, v);
+            off += (ix + a + 1 == n) ? nn - (int64_t)n * nn : nn;   // x wraps once (w <= n)
         }
 #pragma unroll
         for (int a = 0; a < 8; ++a) {
@@ -638,6 +641,41 @@ __device__ __forceinline__ void gather_sub_d(WarpChunk &st, GatherPartials &gp,
         for (int d = 0; d < 3; ++d) {
             gp.D[d][j + r][2 * c4] = Dh[0][d][0] + Dh[1][d][0];
             gp.D[d][j + r][2 * c4 + 1] = Dh[0][d][1] + Dh[1][d][1];
+        }
+    }
+}
+
+// A sub-batch of m < 8 particles without the tensor cores: lane (r, c4) adds
+// its window entries (b = r, slots c4 and c4 + 4) weighted by wx and wz for each
+// particle and the 4 lanes of row r reduce, giving the same D_d[p][b] as
+// gather_sub_d.  Pipe cost ~54 FMAs per particle against 48 DMMAs per
+// sub-batch, so partial sub-batches (cell tails, sparse cells) run here.
+__device__ __forceinline__ void gather_sub_fma(WarpChunk &st, GatherPartials &gp,
+                                               const double (&g)[8][2][3], int j, int m, int k,
+                                               int r, int c4) {
+    const int s0 = (c4 - k) & 7, s1 = (c4 + 4 - k) & 7;
+    for (int q = j; q < j + m; ++q) {
+        double h0[3] = {0.0, 0.0, 0.0}, h1[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const double xa = st.wx[a][q];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                h0[d] = fma(g[a][0][d], xa, h0[d]);
+                h1[d] = fma(g[a][1][d], xa, h1[d]);
+            }
+        }
+        const double z0 = st.wz[q][s0], z1 = st.wz[q][s1];
+        double e[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            e[d] = fma(h1[d], z1, h0[d] * z0);
+            e[d] += __shfl_xor_sync(kFull, e[d], 1);
+            e[d] += __shfl_xor_sync(kFull, e[d], 2);
+        }
+        if (c4 == 0) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) gp.D[d][q][r] = e[d];
         }
     }
 }
@@ -988,6 +1026,11 @@ interp_ws_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
 #ifndef PIF_GATHER_DEFER
 #define PIF_GATHER_DEFER 1
 #endif
+// sub-batches of at most this many particles take the FMA path
+#ifndef PIF_GATHER_FMA_MAX
+#define PIF_GATHER_FMA_MAX 3
+#endif
+constexpr int kGatherFmaMax = PIF_GATHER_FMA_MAX;
 
 #ifndef PIF_GATHER_WARPS
 #define PIF_GATHER_WARPS 4
@@ -1141,7 +1184,8 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                 const int m = min(8, min(pos + cnt, cell_end) - gp);
                 PIF_CHECK(m > 0 && j + m <= kChunk && k >= k0 && k < k1);
 #if PIF_GATHER_DEFER
-                gather_sub_d(st, gpart, g, j, m, k, r, c4);
+                if (m <= kGatherFmaMax) gather_sub_fma(st, gpart, g, j, m, k, r, c4);
+                else gather_sub_d(st, gpart, g, j, m, k, r, c4);
 #else
                 gather_sub(st, g, j, m, k, r, c4);
 #endif
