@@ -168,6 +168,18 @@ int pif_interp_perm(pif_plan_t plan, const pif_soa_t *parts, const int32_t *perm
  * id0 .. id0+M-1); v_out may be NULL. */
 int pif_soa_to_aos(pif_plan_t plan, const pif_soa_t *parts, int64_t id0, double *x_out,
                    double *v_out, void *stream);
+/* Complex type 1 / type 2 on the binned fast kernels (cell-sorted points from
+ * pif_bin_scatter, strengths / outputs indexed by point id):
+ * pif_type1_complex_sorted: modes = type1 of s_re + i s_im (two production
+ * spreads, one C2C FFT; replaces spread_c, _kernels.py:31-54, nufft.py:132-145).
+ * pif_type2_complex_sorted: E_out[3 id + {0, 1}] = (Re, Im) of the type-2 value
+ * at point id (C2C inverse FFT, production gather; replaces interp_c,
+ * _kernels.py:99-122, nufft.py:159-172).  Both overwrite the plan's grids. */
+int pif_type1_complex_sorted(pif_plan_t plan, const pif_soa_t *sorted, const double *s_re,
+                             const double *s_im, double *modes, void *stream);
+int pif_type2_complex_sorted(pif_plan_t plan, const double *modes, const pif_soa_t *sorted,
+                             double *E_out, void *stream);
+
 /* Spread -> gather weight cache.  The gather of a PD step runs at the positions
  * the previous step's deposit spread (strategies.py:290-300: solve(x_n+1), then
  * gather(x_n+1)), in the same perm order and chunking.  When enabled, the

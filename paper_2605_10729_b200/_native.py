@@ -78,6 +78,8 @@ SIGNATURES = {
     "pif_load_aos": ([_P, _P, _P, _I64, _SOA, _P, _P, _P], _I),
     "pif_set_id_order_output": ([_P, _P, _P, _I64], _I),
     "pif_set_weight_cache": ([_P, _I], _I),
+    "pif_type1_complex_sorted": ([_P, _SOA, _P, _P, _P, _P], _I),
+    "pif_type2_complex_sorted": ([_P, _P, _SOA, _P, _P], _I),
     "pif_sample_landau_axis": ([_P, _P, _I64, _I64, _D, _D, _D, _P, _I64, _P, _P], _I),
     "pif_sample_normal": ([_P, _P, _I64, _I64, _I64, _D, _D, _I, _D, _P, _I64, _P, _P], _I),
 }

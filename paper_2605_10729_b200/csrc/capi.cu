@@ -516,4 +516,20 @@ int pif_type2_complex(pif_plan_t plan, const double *modes, const double *pts, i
     return pif::launch_type2_complex(p, modes, pts, M, out, s);
 }
 
+int pif_type1_complex_sorted(pif_plan_t plan, const pif_soa_t *sorted, const double *s_re,
+                             const double *s_im, double *modes, void *stream) {
+    PLAN_CHECK();
+    if (!pif::soa_ok(sorted, false) || !modes) return pif::bad("invalid type1 arguments");
+    if (sorted->count > 0 && (!s_re || !s_im)) return pif::bad("missing strengths");
+    return pif::launch_type1_complex_sorted(p, *sorted, s_re, s_im, modes, s);
+}
+
+int pif_type2_complex_sorted(pif_plan_t plan, const double *modes, const pif_soa_t *sorted,
+                             double *E_out, void *stream) {
+    PLAN_CHECK();
+    if (!pif::soa_ok(sorted, false) || !modes) return pif::bad("invalid type2 arguments");
+    if (sorted->count > 0 && !E_out) return pif::bad("null output");
+    return pif::launch_type2_complex_sorted(p, modes, *sorted, E_out, s);
+}
+
 }  // extern "C"

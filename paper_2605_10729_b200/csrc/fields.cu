@@ -365,6 +365,81 @@ int launch_type1_complex(Plan &p, const double *pts, const double *vals, int64_t
     return fail_cuda(cudaGetLastError(), "modes_from_full_kernel");
 }
 
+__global__ void complex_part_kernel(const double *__restrict__ grid, double2 *__restrict__ cgrid,
+                                    int part, int64_t n3) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n3;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (part) cgrid[i].y = grid[i];
+        else cgrid[i].x = grid[i];
+    }
+}
+
+__global__ void pack_complex_field_kernel(const double2 *__restrict__ cgrid,
+                                          double4 *__restrict__ field, int64_t n3) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n3;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double2 c = cgrid[i];
+        field[i] = make_double4(c.x, c.y, 0.0, 0.0);
+    }
+}
+
+// Complex-strength type 1 on the binned fast path: spread the real and the
+// imaginary strengths with the production spreader (two passes over the same
+// cell-sorted points), interleave into the complex grid, C2C forward FFT,
+// truncate / deconvolve (replaces spread_c + fftn, _kernels.py:31-54,
+// nufft.py:132-145).
+int launch_type1_complex_sorted(Plan &p, const pif_soa_t &sorted, const double *s_re,
+                                const double *s_im, double *modes, cudaStream_t s) {
+    int rc = ensure_complex(p);
+    if (rc != PIF_OK) return rc;
+    const double *parts[2] = {s_re, s_im};
+    for (int part = 0; part < 2; ++part) {
+        rc = launch_spread(p, sorted, nullptr, parts[part], 0.0, s);
+        if (rc != PIF_OK) return rc;
+        complex_part_kernel<<<blocks_for(p.n3, 256, p.sm_count), 256, 0, s>>>(p.grid, p.cgrid,
+                                                                              part, p.n3);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return fail_cuda(e, "complex_part_kernel");
+    }
+    cufftResult r = cufftSetStream(p.z2z, s);
+    if (r == CUFFT_SUCCESS)
+        r = cufftExecZ2Z(p.z2z, reinterpret_cast<cufftDoubleComplex *>(p.cgrid),
+                         reinterpret_cast<cufftDoubleComplex *>(p.cgrid), CUFFT_FORWARD);
+    if (r != CUFFT_SUCCESS) return fail_cufft(r, "cufftExecZ2Z forward");
+    const int64_t N3 = (int64_t)p.N * p.N * p.N;
+    modes_from_full_kernel<<<blocks_for(N3, 256, p.sm_count), 256, 0, s>>>(
+        p.cgrid, p.deconv, reinterpret_cast<double2 *>(modes), p.N, p.n, 1.0 / (double)p.n3);
+    return fail_cuda(cudaGetLastError(), "modes_from_full_kernel");
+}
+
+// Complex type 2 on the binned fast path: padded spectrum, C2C inverse FFT,
+// (Re, Im) packed as two components of the gather's double4 field, then the
+// production gather (interp_c, _kernels.py:99-122): E_out[3 id + {0, 1}] =
+// (Re, Im) of the value at point id.
+int launch_type2_complex_sorted(Plan &p, const double *modes, const pif_soa_t &sorted,
+                                double *E_out, cudaStream_t s) {
+    int rc = ensure_complex(p);
+    if (rc != PIF_OK) return rc;
+    pad_full_kernel<<<blocks_for(p.n3, 256, p.sm_count), 256, 0, s>>>(
+        reinterpret_cast<const double2 *>(modes), p.deconv, p.cgrid, p.N, p.n,
+        1.0 / (double)p.n3);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail_cuda(e, "pad_full_kernel");
+    cufftResult r = cufftSetStream(p.z2z, s);
+    if (r == CUFFT_SUCCESS)
+        r = cufftExecZ2Z(p.z2z, reinterpret_cast<cufftDoubleComplex *>(p.cgrid),
+                         reinterpret_cast<cufftDoubleComplex *>(p.cgrid), CUFFT_INVERSE);
+    if (r != CUFFT_SUCCESS) return fail_cufft(r, "cufftExecZ2Z inverse");
+    pack_complex_field_kernel<<<blocks_for(p.n3, 256, p.sm_count), 256, 0, s>>>(
+        p.cgrid, reinterpret_cast<double4 *>(p.field), p.n3);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return fail_cuda(e, "pack_complex_field_kernel");
+    p.field_valid = true;
+    pif_soa_t v = sorted;
+    return launch_interp(p, v, nullptr, v, false, 0.0, 1.0, nullptr, nullptr, 0, PIF_EXT_NONE,
+                         nullptr, nullptr, nullptr, E_out, s);
+}
+
 int launch_type2_complex(Plan &p, const double *modes, const double *pts, int64_t M,
                          double *out, cudaStream_t s) {
     int rc = ensure_complex(p);

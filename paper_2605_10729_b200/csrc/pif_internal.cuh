@@ -112,6 +112,10 @@ int launch_bin_perm(Plan &p, const int32_t *key, const int32_t *rank, int64_t M,
 int launch_spread(Plan &p, const pif_soa_t &parts, const int32_t *perm, const double *strengths,
                   double q, cudaStream_t s);
 int ensure_wcache(Plan &p, int64_t M);
+int launch_type1_complex_sorted(Plan &p, const pif_soa_t &sorted, const double *s_re,
+                                const double *s_im, double *modes, cudaStream_t s);
+int launch_type2_complex_sorted(Plan &p, const double *modes, const pif_soa_t &sorted,
+                                double *E_out, cudaStream_t s);
 int launch_load_aos(Plan &p, const double *x, const double *v, int64_t id0, pif_soa_t &dst,
                     int32_t *key, int32_t *rank, cudaStream_t s);
 int launch_interp(Plan &p, const pif_soa_t &src, const int32_t *perm, pif_soa_t &dst, bool push,

@@ -231,9 +231,10 @@ def type1(plan: NufftPlan, points, strengths) -> FourierField:
                      s.data_ptr(), 0.0, stream)
         _native.call("pif_grid_to_modes", dp.handle, modes.data_ptr(), stream)
     else:
-        aos = _wrapped_aos(plan, pts)
-        _native.call("pif_type1_complex", dp.handle, aos.data_ptr(), s.data_ptr(), M,
-                     modes.data_ptr(), stream)
+        sp = SortedPoints(plan, pts)
+        s_re, s_im = s.real.contiguous(), s.imag.contiguous()
+        _native.call("pif_type1_complex_sorted", dp.handle, _native.ctypes.byref(sp.view),
+                     s_re.data_ptr(), s_im.data_ptr(), modes.data_ptr(), stream)
     return FourierField(N, plan.L, like_input(modes, points))
 
 
@@ -255,10 +256,13 @@ def type2(plan: NufftPlan, modes, points):
     c = _coeffs_of(plan, modes)
     pts = _points_device(points).to(c.device)
     M = int(pts.shape[0])
-    out = torch.empty(M, dtype=torch.complex128, device=c.device)
-    aos = _wrapped_aos(plan, pts)
-    _native.call("pif_type2_complex", plan.native(c.device).handle, c.data_ptr(),
-                 aos.data_ptr(), M, out.data_ptr(), _native.stream_handle(c.device))
+    if M == 0:
+        return like_input(torch.empty(0, dtype=torch.complex128, device=c.device), points)
+    E = torch.zeros((M, 3), dtype=torch.float64, device=c.device)
+    sp = SortedPoints(plan, pts)
+    _native.call("pif_type2_complex_sorted", plan.native(c.device).handle, c.data_ptr(),
+                 _native.ctypes.byref(sp.view), E.data_ptr(), _native.stream_handle(c.device))
+    out = torch.complex(E[:, 0].contiguous(), E[:, 1].contiguous())
     return like_input(out, points)
 
 

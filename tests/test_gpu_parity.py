@@ -700,3 +700,19 @@ def test_engine_handles_empty_and_ragged_particle_sets(count, cuda):
     xo, vo = o.boris_push(x.copy(), v.copy(), Eo, -0.01, 0.01, (0.0, 0.0, 0.0), "none", 0.05, L)
     assert rel_max(vg.cpu().numpy(), vo) <= 1e-12
     assert rel_max(xg.cpu().numpy(), xo) <= 1e-12
+
+
+@pytest.mark.parametrize("eps", [1e-6, 1e-12])
+def test_complex_transforms_on_binned_kernels_at_density(eps):
+    """Complex type 1 / type 2 (spread_c / interp_c) through the binned fast
+    kernels at ~16 points per stencil cell: against the oracle."""
+    o = oracle()
+    N, L, M = 8, 2 * np.pi, 65536
+    plan, op = pb.make_plan(N, L, eps), o.make_plan(N, L, eps)
+    rng = np.random.default_rng(77)
+    x = rng.random((M, 3)) * L
+    c = rng.standard_normal(M) + 1j * rng.standard_normal(M)
+    assert rel_l2(pb.type1(plan, x, c).coeffs, o.type1(op, x, c)) <= TIGHT
+    f = rng.standard_normal((N,) * 3) + 1j * rng.standard_normal((N,) * 3)
+    assert rel_l2(pb.type2(plan, f, x), o.type2(op, f, x)) <= TIGHT
+    assert pb.type2(plan, f, np.zeros((0, 3))).shape == (0,)

@@ -101,9 +101,22 @@ def run_case(N, M, eps, kind, reps):
     ts = timed(spread_only, reps)
     t2 = timed(type2, reps)
     tg = timed(gather_only, reps)
-    del eng, x, v, ids, E
+    del eng, v, ids, E
     torch.cuda.empty_cache()
-    return dict(N=N, M=M, eps=eps, w=w, kind=kind, t1=t1, ts=ts, t2=t2, tg=tg,
+    # complex-strength type 1 / complex type 2 through the public API
+    # (pb.type1 / pb.type2 on device tensors: binning + 2 spreads + C2C, or
+    # C2C + gather, per call)
+    cs = torch.complex(torch.randn(M, generator=rng, dtype=torch.float64, device="cuda"),
+                       torch.randn(M, generator=rng, dtype=torch.float64, device="cuda"))
+    fc = torch.complex(torch.randn((N, N, N), generator=rng, dtype=torch.float64, device="cuda"),
+                       torch.randn((N, N, N), generator=rng, dtype=torch.float64, device="cuda"))
+    pb.type1(plan, x, cs)
+    pb.type2(plan, fc, x)
+    t1c = timed(lambda: pb.type1(plan, x, cs), reps)
+    t2c = timed(lambda: pb.type2(plan, fc, x), reps)
+    del x, cs
+    torch.cuda.empty_cache()
+    return dict(N=N, M=M, eps=eps, w=w, kind=kind, t1=t1, ts=ts, t2=t2, tg=tg, t1c=t1c, t2c=t2c,
                 fs=(2 * w ** 3 + w ** 2), fg=(6 * w ** 3 + w ** 2), modes=Ns)
 
 
@@ -120,8 +133,8 @@ def main():
     print(f"B200, fp64, FP64 peak measured live: {peak:.1f} TF/s. type-1 = bin + spread + "
           "D2Z + truncate; type-2 = padded Z2D (3 comps) + gather. Points/s = M / time.\n")
     print("| modes | points | eps (w) | layout | type-1 pts/s | spread | spread % FP64 | "
-          "type-2 pts/s | gather | gather % FP64 |")
-    print("|---|---|---|---|---:|---:|---:|---:|---:|---:|")
+          "type-2 pts/s | gather | gather % FP64 | complex type-1 pts/s | complex type-2 pts/s |")
+    print("|---|---|---|---|---:|---:|---:|---:|---:|---:|---:|---:|")
     for eps in epss:
         for N in Ns:
             for M in Ms:
@@ -134,7 +147,8 @@ def main():
                     gp = M * r["fg"] / r["tg"] / 1e12 / peak * 100
                     print(f"| {N}^3 | 2^{int(math.log2(M))} | {eps:g} ({r['w']}) | {kind} | "
                           f"{M / r['t1']:.3g} | {r['ts'] * 1e3:.2f} ms | {sp:.1f}% | "
-                          f"{M / r['t2']:.3g} | {r['tg'] * 1e3:.2f} ms | {gp:.1f}% |", flush=True)
+                          f"{M / r['t2']:.3g} | {r['tg'] * 1e3:.2f} ms | {gp:.1f}% | "
+                          f"{M / r['t1c']:.3g} | {M / r['t2c']:.3g} |", flush=True)
 
 
 if __name__ == "__main__":
