@@ -358,11 +358,23 @@ def run_b200(a):
 
 def run_e2e(a, eng, torch, dist, world, per_gpu, glob, dev):
     """pif_step-style use with host (pinned) particle arrays in id order (the
-    reference's ParticleEnsemble layout): per step H2D of x, v (ids implied by
-    position), upload + wrap + bin, spread, D2Z, allreduce, fields,
-    gather+push, device scatter back to id order, D2H of x, v and the field
-    energy."""
+    reference's ParticleEnsemble layout) through PifEngine.run_host: per step
+    H2D of x, v (ids implied by position), fused load + bin, spread, D2Z,
+    allreduce, fields, gather+push writing x, v in id order, D2H of x, v and
+    the field energy.  Every rank of the node pins 96 B per particle; if the
+    host cannot hold that the line says so instead of failing the run."""
     M = eng.count
+    need = 96 * M * int(os.environ.get("LOCAL_WORLD_SIZE", world))
+    try:
+        import psutil
+        avail = psutil.virtual_memory().available
+    except Exception:  # noqa: BLE001
+        avail = None
+    if avail is not None and need > 0.8 * avail:
+        return {"value": None, "unit": UNIT, "h2d_bytes_per_step": M * 48 * world,
+                "d2h_bytes_per_step": (M * 48 + 8) * world,
+                "skipped": f"host memory: {need / 1e9:.0f} GB pinned needed, "
+                           f"{avail / 1e9:.0f} GB available"}
     lo = int(eng.parts.ids[eng.parts.cur][:M].min())
     xh = torch.empty((M, 3), dtype=torch.float64, pin_memory=True)
     vh = torch.empty((M, 3), dtype=torch.float64, pin_memory=True)
