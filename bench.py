@@ -166,11 +166,14 @@ def run_reference(a):
     if rank != 0:
         return
     cfg, w, per_gpu, glob = workload_config(a, world)
-    steps = max(1, min(a.steps, 4))
-    val, cores, sample, sec = cpu_reference_run(a, a.cpu_particles, steps, min(a.warmup, 1))
+    # K timed steps after W warm-ups, each a bounded sample (cpu_particles) of the
+    # workload; capped so a long GPU-side K still ends within a couple of minutes
+    steps = max(1, min(a.steps, 30))
+    warm = max(0, min(a.warmup, 3))
+    val, cores, sample, sec = cpu_reference_run(a, a.cpu_particles, steps, warm)
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
-        "steps": steps, "warmup": min(a.warmup, 1), "ms_per_step": sec * 1e3,
+        "steps": steps, "warmup": warm, "ms_per_step": sec * 1e3,
         "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference samplers, seed 0)", "config": cfg,
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
