@@ -716,3 +716,28 @@ def test_complex_transforms_on_binned_kernels_at_density(eps):
     f = rng.standard_normal((N,) * 3) + 1j * rng.standard_normal((N,) * 3)
     assert rel_l2(pb.type2(plan, f, x), o.type2(op, f, x)) <= TIGHT
     assert pb.type2(plan, f, np.zeros((0, 3))).shape == (0,)
+
+
+@pytest.mark.parametrize("N", [4, 6])
+def test_smallest_grids_where_the_window_wraps_the_domain(N):
+    """N = 4 (n = 8 = w: the footprint covers the periodic grid) and N = 6
+    (n = 12): type 1, the 3-component gather and one engine step vs the oracle."""
+    o = oracle()
+    L, M = 2 * np.pi, 3000
+    plan, op = pb.make_plan(N, L, 1e-7), o.make_plan(N, L, 1e-7)
+    rng = np.random.default_rng(N)
+    x = rng.random((M, 3)) * L
+    q = rng.standard_normal(M)
+    assert rel_l2(pb.type1(plan, x, q).coeffs, o.type1(op, x, q)) <= TIGHT
+    herm = [np.fft.fftshift(np.fft.fftn(rng.standard_normal((N,) * 3))) / N ** 3 for _ in range(3)]
+    assert rel_l2(nufft.gather3_real(plan, herm, x), o.gather3_real(op, herm, x)) <= TIGHT
+    v = rng.standard_normal((M, 3))
+    ens = _ens(x, v, q=-1.0 / M, m=1.0 / M)
+    st = pb.pif_step(pb.StepState(ensemble=ens, plan=plan, externals=pb.ExternalFieldsSpec(L=L),
+                                  dt=0.05))
+    rho = o.deposit_charge(x, -1.0 / M, op)
+    Eo = o.gather_efield(o.poisson_efield(rho, L), x, op)
+    xo, vo = o.boris_push(x.copy(), v.copy(), Eo, -1.0 / M, 1.0 / M, (0.0, 0.0, 0.0), "none",
+                          0.05, L)
+    assert rel_max(st.ensemble.v, vo) <= 1e-12
+    assert rel_max(st.ensemble.x, xo) <= 1e-12
