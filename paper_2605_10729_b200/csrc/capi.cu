@@ -200,7 +200,6 @@ int pif_plan_create(const pif_plan_desc_t *d, int device, pif_plan_t *out) {
     cudaDeviceGetAttribute(&p.sm_count, cudaDevAttrMultiProcessorCount, device);
     p.partial_blocks = p.sm_count * 32;
     pif::build_es_poly(p.w, p.beta, &p.poly, &p.poly_err);
-    if (const char *ws = std::getenv("PIF_INTERP_WS")) p.interp_ws = std::atoi(ws) != 0;
     if (const char *fg = std::getenv("PIF_FORCE_GENERIC")) p.force_generic = std::atoi(fg) != 0;
     if (const char *st = std::getenv("PIF_SEG_TARGET")) p.seg_target = std::max(1, std::atoi(st));
     if (const char *fr = std::getenv("PIF_FORCE_RING")) p.force_ring = std::atoi(fr) != 0;

@@ -555,61 +555,9 @@ __device__ __forceinline__ void load_plane(double (&g)[8][2][3], int hh, const d
 // lane (r, c4) holding E(a, b=r, slot c4+4h) is a valid B fragment):
 //   A_{a,h}[p][c'] = wx_p[a] wz_p[(c' + 4h - k) mod 8]    (p = r)
 //   D_d[p][b]     += A_{a,h} x B_{a,h,d}[c'][b]           (16 DMMAs per component)
-// then E_d(p) = sum_b wy_p[b] D_d[p][b]: one product pair per lane and a
-// 2-level butterfly over the 4 lanes sharing p.
-__device__ __forceinline__ void gather_sub(WarpChunk &st, const double (&g)[8][2][3], int j, int m,
-                                           int k, int r, int c4) {
-    const int pb = r < m ? j + r : j;
-    const double sc = r < m ? 1.0 : 0.0;
-    const double bz0 = sc * st.wz[pb][(c4 - k) & 7];
-    const double bz1 = sc * st.wz[pb][(c4 + 4 - k) & 7];
-    // all 16 A operands first (distinct registers: no write-after-read wait on
-    // operands still being consumed by in-flight DMMAs), then 48 DMMAs over 6
-    // independent accumulator chains D[h][d]
-    double A[8][2];
-#pragma unroll
-    for (int a = 0; a < 8; ++a) {
-        const double wxa = st.wx[a][pb];
-        A[a][0] = wxa * bz0;
-        A[a][1] = wxa * bz1;
-    }
-    double Dh[2][3][2];
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh)
-#pragma unroll
-        for (int d = 0; d < 3; ++d) Dh[hh][d][0] = Dh[hh][d][1] = 0.0;
-#pragma unroll
-    for (int a = 0; a < 8; ++a)
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh)
-#pragma unroll
-            for (int d = 0; d < 3; ++d)
-                dmma884(Dh[hh][d][0], Dh[hh][d][1], A[a][hh], g[a][hh][d]);
-    double D[3][2];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        D[d][0] = Dh[0][d][0] + Dh[1][d][0];
-        D[d][1] = Dh[0][d][1] + Dh[1][d][1];
-    }
-    const double wy0 = st.wy[pb][2 * c4], wy1 = st.wy[pb][2 * c4 + 1];
-    double e[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) e[d] = fma(wy1, D[d][1], wy0 * D[d][0]);
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        e[d] += __shfl_xor_sync(kFull, e[d], 1);
-        e[d] += __shfl_xor_sync(kFull, e[d], 2);
-    }
-    if (c4 == 0 && r < m) {
-        st.E[0][j + r] = e[0];
-        st.E[1][j + r] = e[1];
-        st.E[2][j + r] = e[2];
-    }
-}
-
-// As gather_sub, but the 8 x 8 result D_d[p][b] of the sub-batch goes to
-// shared memory; E_d(p) = sum_b wy_p[b] D_d[p][b] is formed later by lane p
-// (gather_reduce), off the DMMA loop's critical path.
+// The 8 x 8 result D_d[p][b] of the sub-batch goes to shared memory;
+// E_d(p) = sum_b wy_p[b] D_d[p][b] is formed later by lane p (gather_reduce),
+// off the DMMA loop's critical path.
 __device__ __forceinline__ void gather_sub_d(WarpChunk &st, GatherPartials &gp,
                                              const double (&g)[8][2][3], int j, int m, int k,
                                              int r, int c4) {
@@ -681,7 +629,7 @@ __device__ __forceinline__ void gather_sub_fma(WarpChunk &st, GatherPartials &gp
 }
 
 // E of this lane's particle p from its partial sums (same pairing as the
-// shuffle tree of gather_sub: ((b0 b1 + b2 b3) + (b4 b5 + b6 b7)))
+// pairwise tree ((b0 b1 + b2 b3) + (b4 b5 + b6 b7)))
 __device__ __forceinline__ void gather_reduce(const WarpChunk &st, const GatherPartials &gp, int p,
                                               double (&E)[3]) {
     double wy[8];
@@ -743,288 +691,8 @@ __device__ unsigned long long g_phase_cycles[8];
 #define PHASE_ADD(slot, a, b)
 #endif
 
-// ----------------------------------------------------------------------------
-// warp-specialised gather + push (w <= 8): one 64-thread block = a pair
-//   warp 0 (particle warp): fetches work items, loads particles through perm
-//           (one chunk ahead), computes window weights into a double-buffered
-//           stage, and pushes chunk c-2 once its fields are back;
-//   warp 1 (MMA warp): keeps the cell's field window in registers and runs the
-//           DMMA gather of each staged chunk, writing E to the stage.
-// Named barriers: READY_b (particle -> MMA, stage b filled), EDONE_b (MMA ->
-// particle, E of stage b written).  Neither warp holds both the 96-register
-// window and the weight/push temporaries, so more pairs fit per SM.
-// ----------------------------------------------------------------------------
-
-struct PairMeta {
-    int ix, iy, k0, k1, kf, pos, cnt, new_item;
-    int cb[12];   // cell boundaries of the item's z-segment (seg <= 11)
-};
-
-struct PairShared {
-    WarpChunk stage[2];
-    double4 planes[8][8];
-    PairMeta meta[2];
-    double tab[32];
-};
-
-// barrier ids as immediates (a register id makes ptxas reserve all 16 named
-// barriers per CTA, which caps the CTAs per SM)
-__device__ __forceinline__ void named_sync(int id) {
-    switch (id) {
-        case 1: asm volatile("bar.sync 1, 64;" ::: "memory"); break;
-        case 2: asm volatile("bar.sync 2, 64;" ::: "memory"); break;
-        case 3: asm volatile("bar.sync 3, 64;" ::: "memory"); break;
-        default: asm volatile("bar.sync 4, 64;" ::: "memory"); break;
-    }
-}
-__device__ __forceinline__ void named_arrive(int id) {
-    switch (id) {
-        case 1: asm volatile("bar.arrive 1, 64;" ::: "memory"); break;
-        case 2: asm volatile("bar.arrive 2, 64;" ::: "memory"); break;
-        case 3: asm volatile("bar.arrive 3, 64;" ::: "memory"); break;
-        default: asm volatile("bar.arrive 4, 64;" ::: "memory"); break;
-    }
-}
-constexpr int kBarReady = 1, kBarEdone = 3;   // ids 1,2 and 3,4
-
-struct ParticleRegs {
-    double x, y, z, vx, vy, vz;
-    int64_t id;
-};
-
-template <int W>
-__device__ __forceinline__ void ws_particle_warp(PairShared &sh, const pif_soa_t &P,
-                                                 const int32_t *__restrict__ perm, pif_soa_t &Q,
-                                                 const int32_t *__restrict__ cell_start,
-                                                 int seg, int nseg, double beta,
-                                                 const EsPoly &poly, const PushParams &pp,
-                                                 int32_t *__restrict__ key,
-                                                 int32_t *__restrict__ rank,
-                                                 int32_t *__restrict__ count, unsigned int *work,
-                                                 const int2 *__restrict__ items, int nitems,
-                                                 double *dg) {
-    const int lane = threadIdx.x & 31;
-    const int n = pp.n;
-    const double h = pp.h;
-    ParticleRegs held0{0, 0, 0, 0, 0, 0, 0}, held1{0, 0, 0, 0, 0, 0, 0};  // stages 0/1
-    int held_pos0 = 0, held_pos1 = 0, held_cnt0 = 0, held_cnt1 = 0;
-    int c = 0;                       // chunks published
-    int64_t rank_idx = -1;
-    int rank_val = 0;
-#ifdef PIF_PHASE_TIMING
-    unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#endif
-
-    auto push_stage = [&](int b) {
-        const WarpChunk &st = sh.stage[b];
-        if (rank_idx >= 0) {
-            rank[rank_idx] = rank_val;
-            rank_idx = -1;
-        }
-        const int hc = b ? held_cnt1 : held_cnt0;
-        if (lane < hc) {
-            const int64_t i = (b ? held_pos1 : held_pos0) + lane;
-            ParticleRegs q = b ? held1 : held0;
-            boris_one(pp, st.E[0][lane], st.E[1][lane], st.E[2][lane], q.x, q.y, q.z, q.vx, q.vy,
-                      q.vz, dg);
-            Q.x[i] = q.x; Q.y[i] = q.y; Q.z[i] = q.z;
-            Q.vx[i] = q.vx; Q.vy[i] = q.vy; Q.vz[i] = q.vz;
-            if (perm) Q.id[i] = q.id;
-            const int kk = cell_key(q.x, q.y, q.z, h, pp.rh, pp.w, n);
-            PIF_CHECK(kk >= 0 && kk < n * n * n);
-            key[i] = kk;
-            rank_val = atomicAdd(&count[kk], 1);
-            rank_idx = i;
-        }
-    };
-
-    for (;;) {
-        int item = 0;
-        if (lane == 0) item = (int)atomicAdd(work, 1u);
-        item = __shfl_sync(kFull, item, 0);
-        if (item >= nitems) break;
-        const int2 it = items[item];
-        const int col = it.x / nseg, sg = it.x - col * nseg;
-        const int ix = col / n, iy = col - ix * n;
-        const int k0 = sg * seg, k1 = min(k0 + seg, n);
-        const int base = col * n;
-        const int cb = cell_start[base + k0 + min(lane, k1 - k0)];
-        const int pbeg = __shfl_sync(kFull, cb, 0) + it.y * kItemParticles;
-        const int pend = min(pbeg + kItemParticles, __shfl_sync(kFull, cb, k1 - k0));
-        int kf = k0;
-        while (__shfl_sync(kFull, cb, kf - k0 + 1) <= pbeg) ++kf;
-
-        ParticleRegs nxt{0, 0, 0, 0, 0, 0, 0};
-        if (pbeg + lane < pend) {
-            const int i = perm ? perm[pbeg + lane] : pbeg + lane;
-            nxt = {P.x[i], P.y[i], P.z[i], P.vx[i], P.vy[i], P.vz[i], perm ? P.id[i] : 0};
-        }
-        for (int pos = pbeg; pos < pend; pos += kChunk) {
-            const int b = c & 1;
-            const int cnt = min(kChunk, pend - pos);
-            const ParticleRegs cur = nxt;
-            if (pos + kChunk + lane < pend) {   // prefetch the next chunk
-                const int i = perm ? perm[pos + kChunk + lane] : pos + kChunk + lane;
-                nxt = {P.x[i], P.y[i], P.z[i], P.vx[i], P.vy[i], P.vz[i], perm ? P.id[i] : 0};
-            }
-            PHASE_MARK(t0);
-            if (c >= 2) {   // stage b still holds chunk c-2: wait for its E, push it
-                named_sync(kBarEdone + b);
-                PHASE_MARK(t1);
-                PHASE_ADD(2, t0, t1);
-                push_stage(b);
-                PHASE_MARK(t2);
-                PHASE_ADD(1, t1, t2);
-            }
-            PHASE_MARK(t3);
-            chunk_weights<W, true>(sh.stage[b], sh.tab, poly, lane, cnt, cur.x, cur.y, cur.z, 1.0,
-                                   false, h, pp.rh, beta);
-            PHASE_MARK(t4);
-            PHASE_ADD(0, t3, t4);
-            if (b) {
-                held1 = cur;
-                held_pos1 = pos;
-                held_cnt1 = cnt;
-            } else {
-                held0 = cur;
-                held_pos0 = pos;
-                held_cnt0 = cnt;
-            }
-            if (lane == 0) {
-                PairMeta &m = sh.meta[b];
-                m.ix = ix; m.iy = iy; m.k0 = k0; m.k1 = k1; m.kf = kf;
-                m.pos = pos; m.cnt = cnt; m.new_item = pos == pbeg;
-            }
-            if (lane <= k1 - k0) sh.meta[b].cb[lane] = cb;
-            __syncwarp();
-            named_arrive(kBarReady + b);
-            ++c;
-        }
-    }
-    // sentinel, then drain the last two chunks
-    {
-        const int b = c & 1;
-        if (c >= 2) {
-            named_sync(kBarEdone + b);
-            push_stage(b);
-        }
-        if (lane == 0) sh.meta[b].cnt = -1;
-        __syncwarp();
-        named_arrive(kBarReady + b);
-        if (c >= 1) {
-            named_sync(kBarEdone + (b ^ 1));
-            push_stage(b ^ 1);
-        }
-    }
-    if (rank_idx >= 0) rank[rank_idx] = rank_val;
-#ifdef PIF_PHASE_TIMING
-    ph[5] = c;
-    if (lane == 0)
-        for (int i = 0; i < 6; ++i) atomicAdd(&g_phase_cycles[i], ph[i]);
-#endif
-}
-
-__device__ __forceinline__ void ws_mma_warp(PairShared &sh, const double4 *__restrict__ field,
-                                            int n) {
-#ifdef PIF_PHASE_TIMING
-    unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#endif
-    const int lane = threadIdx.x & 31;
-    const int r = lane >> 2, c4 = lane & 3;
-    double g[8][2][3];
-    int ix = 0, iy = 0, k0 = 0, k = 0, cell_end = 0;
-    int64_t yrow = 0;
-    for (int c = 0;; ++c) {
-        const int b = c & 1;
-        PHASE_MARK(t0);
-        named_sync(kBarReady + b);
-        PHASE_MARK(t1);
-        PHASE_ADD(7, t0, t1);
-        const PairMeta &m = sh.meta[b];
-        const int cnt = m.cnt;
-        if (cnt < 0) break;
-        const int pos = m.pos;
-        if (m.new_item) {
-            ix = m.ix;
-            iy = m.iy;
-            k0 = m.k0;
-            const int kf = m.kf;
-            yrow = (iy + r) % n;
-            prefetch_wait();
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                const int s = c4 + 4 * hh;
-                load_plane(g, hh, field, ix, yrow, n, (kf + ((s - kf) & 7)) % n);
-            }
-            k = kf;
-            cell_end = m.cb[kf - k0 + 1];
-            prefetch_plane(sh.planes, field, ix, iy, n, (kf + 8) % n, lane);
-        }
-        WarpChunk &st = sh.stage[b];
-        int j = 0;
-        while (j < cnt) {
-            const int gp = pos + j;
-            if (gp >= cell_end) {   // next cell: plane k leaves slot k&7, plane k+8 enters
-                const int s = k & 7;
-                prefetch_wait();
-                if (c4 == (s & 3)) {
-                    if (s >> 2) plane_from_smem(g, 1, sh.planes, r);
-                    else plane_from_smem(g, 0, sh.planes, r);
-                }
-                __syncwarp();
-                ++k;
-                prefetch_plane(sh.planes, field, ix, iy, n, (k + 8) % n, lane);
-                cell_end = m.cb[k - k0 + 1];
-                continue;
-            }
-            const int mm = min(8, min(pos + cnt, cell_end) - gp);
-            PIF_CHECK(mm > 0 && j + mm <= kChunk);
-            gather_sub(st, g, j, mm, k, r, c4);
-            j += mm;
-        }
-        __syncwarp();
-        PHASE_MARK(t2);
-        PHASE_ADD(6, t1, t2);
-        named_arrive(kBarEdone + b);
-    }
-    prefetch_wait();
-#ifdef PIF_PHASE_TIMING
-    if (lane == 0)
-        for (int i = 6; i < 8; ++i) atomicAdd(&g_phase_cycles[i], ph[i]);
-#endif
-}
-
-template <int W>
-__global__ void __launch_bounds__(64, 6)
-interp_ws_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
-                 const int32_t *__restrict__ cell_start, const double4 *__restrict__ field,
-                 int seg, int nseg, double beta, const EsPoly poly, PushParams pp,
-                 int32_t *__restrict__ key, int32_t *__restrict__ rank,
-                 int32_t *__restrict__ count, double *__restrict__ partials, unsigned int *work,
-                 const int2 *__restrict__ items, const int *__restrict__ n_items) {
-    __shared__ PairShared sh;
-    const int nitems = *n_items;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (warp == 0) sh.tab[lane] = kExp2Table[lane];
-    if (warp == 0)
-        for (int b = 0; b < 2; ++b) chunk_zero(sh.stage[b], lane);
-    __syncthreads();
-    double dg[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    if (warp == 0) {
-        ws_particle_warp<W>(sh, P, perm, Q, cell_start, seg, nseg, beta, poly, pp, key, rank,
-                            count, work, items, nitems, dg);
-    } else {
-        ws_mma_warp(sh, field, pp.n);
-    }
-    block_diag_store(dg, partials);
-}
-
-
 #ifndef PIF_INTERP_MINB
 #define PIF_INTERP_MINB 2
-#endif
-#ifndef PIF_GATHER_DEFER
-#define PIF_GATHER_DEFER 1
 #endif
 // sub-batches of at most this many particles take the FMA path
 #ifndef PIF_GATHER_FMA_MAX
@@ -1049,16 +717,12 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                   const double *__restrict__ wc, int64_t wstride) {
     const int nitems = *n_items;
     __shared__ WarpChunk stage[kGatherWarps];
-    __shared__ double4 planes[kWarpsPerBlock][8][8];
+    __shared__ double4 planes[kGatherWarps][8][8];
     __shared__ double tab[32];
     extern __shared__ double4 dyn_smem[];
-#if PIF_GATHER_DEFER
     GatherPartials &gpart = reinterpret_cast<GatherPartials *>(dyn_smem)[threadIdx.x >> 5];
     WarpChunk *stage2 = reinterpret_cast<WarpChunk *>(
         reinterpret_cast<GatherPartials *>(dyn_smem) + kGatherWarps);
-#else
-    WarpChunk *stage2 = reinterpret_cast<WarpChunk *>(dyn_smem);
-#endif
     if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -1183,12 +847,8 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                 }
                 const int m = min(8, min(pos + cnt, cell_end) - gp);
                 PIF_CHECK(m > 0 && j + m <= kChunk && k >= k0 && k < k1);
-#if PIF_GATHER_DEFER
                 if (m <= kGatherFmaMax) gather_sub_fma(st, gpart, g, j, m, k, r, c4);
                 else gather_sub_d(st, gpart, g, j, m, k, r, c4);
-#else
-                gather_sub(st, g, j, m, k, r, c4);
-#endif
                 j += m;
             }
             __syncwarp();
@@ -1196,13 +856,9 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
             PHASE_ADD(1, t1, t2);
             if (lane < cnt) {
                 const int64_t i = pos + lane;
-#if PIF_GATHER_DEFER
                 double Eg[3];
                 gather_reduce(st, gpart, lane, Eg);
                 const double E0 = Eg[0], E1 = Eg[1], E2 = Eg[2];
-#else
-                const double E0 = st.E[0][lane], E1 = st.E[1][lane], E2 = st.E[2][lane];
-#endif
                 if (PUSH) {
                     double x = x0, y = y0, z = z0;
                     double vx = vx0, vy = vy0, vz = vz0;
@@ -2043,7 +1699,7 @@ int launch_spread(Plan &p, const pif_soa_t &P, const int32_t *perm, const double
 
 // dynamic shared memory of interp_mma_kernel: the per-warp partial sums (+ the
 // second weight stage when the weight cache is in use)
-constexpr int kGatherDyn = PIF_GATHER_DEFER ? (int)(kGatherWarps * sizeof(GatherPartials)) : 0;
+constexpr int kGatherDyn = (int)(kGatherWarps * sizeof(GatherPartials));
 constexpr int kGatherDynMax = kGatherDyn + (int)(kGatherWarps * sizeof(WarpChunk));
 
 // spread -> gather window-weight cache, [24][M] doubles, grown on demand
@@ -2089,14 +1745,7 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
         const int gthreads = kGatherWarps * 32;
 #define PIF_INTERP_CASE(W)                                                                    \
     case W: {                                                                                 \
-        if (push && p.interp_ws && !pp.mx) {                                                  \
-            auto k = interp_ws_kernel<W>;                                                     \
-            blocks = persistent_blocks(k, 64, 0, p.sm_count);                                 \
-            if (blocks > p.partial_blocks) blocks = p.partial_blocks;                         \
-            k<<<blocks, 64, 0, s>>>(P, perm, Q, p.cell_start, field, p.seg, nseg, p.beta, poly,  \
-                                    pp, key, rank, p.cell_count, p.partials, p.work, p.items, \
-                                    nitems);                                                  \
-        } else if (push) {                                                                    \
+        if (push) {                                                                           \
             auto k = interp_mma_kernel<W, true>;                                             \
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kGatherDynMax); \
             blocks = persistent_blocks(k, gthreads, dyn, p.sm_count);                         \

@@ -85,7 +85,6 @@ struct Plan {
     cufftHandle d2z = 0, z2d3 = 0, z2z = 0;
     bool z2d_strided = false;      // Z2D writes the interleaved grid directly
     bool field_valid = false;
-    bool interp_ws = false;         // warp-specialised gather+push (env PIF_INTERP_WS=1: on)
     bool force_generic = false;
     bool force_ring = false;       // PIF_FORCE_RING: w = 8 through the ring kernels (A/B)     // env PIF_FORCE_GENERIC=1: one-thread-per-particle kernels
     int sm_count = 148;
