@@ -30,6 +30,7 @@ step = -(-M // C)
 bounds = [(i, min(M, i + step)) for i in range(0, M, step)]
 ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 marks = []
+phases = []
 t0 = ev()
 t0.record()
 up.wait_stream(main)
@@ -41,11 +42,15 @@ for s in range(K):
     main.wait_stream(up)
     a = ev(); a.record(main)
     eng.load_aos(xd, vd, 0)
+    a1 = ev(); a1.record(main)
     eng.deposit(); eng.allreduce(); eng.solve_fields()
-    _native.call("pif_set_id_order_output", eng.handle, xd.data_ptr(), vd.data_ptr(), 0)
+    a2 = ev(); a2.record(main)
+    if os.environ.get("NOMIRROR") != "1":
+        _native.call("pif_set_id_order_output", eng.handle, xd.data_ptr(), vd.data_ptr(), 0)
     eng.gather_push()
     _native.call("pif_set_id_order_output", eng.handle, None, None, 0)
     b = ev(); b.record(main)
+    phases.append((a, a1, a2, b))
     down.wait_stream(main)
     last = s == K - 1
     for i0, i1 in bounds:
@@ -61,6 +66,9 @@ for s in range(K):
     d = ev(); d.record(up)
     marks.append((a, b, c, d))
 torch.cuda.synchronize()
+for s, (a, a1, a2, b) in enumerate(phases):
+    print(f"step {s}: load_aos+bin {a.elapsed_time(a1):.1f} ms, deposit+solve {a1.elapsed_time(a2):.1f} ms, "
+          f"gather+push(+mirror) {a2.elapsed_time(b):.1f} ms")
 for s, (a, b, c, d) in enumerate(marks):
     print(f"step {s}: compute start {t0.elapsed_time(a):8.1f}  compute end {t0.elapsed_time(b):8.1f}"
           f"  D2H end {t0.elapsed_time(c):8.1f}  H2D end {t0.elapsed_time(d):8.1f} ms")
