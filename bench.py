@@ -50,7 +50,8 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=None,
+                    help="host-streamed steps in the e2e measurement (default min(--steps, 10))")
     return ap.parse_args()
 
 
@@ -386,12 +387,12 @@ def run_e2e(a, eng, torch, dist, world, per_gpu, glob, dev):
     vh.copy_(vd)
     del xd, vd
 
-    wh = torch.empty(max(1, a.e2e_steps), dtype=torch.float64, pin_memory=True)
+    K = max(1, a.e2e_steps if a.e2e_steps is not None else min(a.steps, 10))
+    wh = torch.empty(K, dtype=torch.float64, pin_memory=True)
     eng.run_host(xh, vh, lo, 1, energy_out=wh)       # warm-up (allocates the staging)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    K = max(1, a.e2e_steps)
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
     eng.run_host(xh, vh, lo, K, energy_out=wh)
