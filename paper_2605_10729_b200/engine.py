@@ -244,8 +244,7 @@ class PifEngine:
         if graph is None:
             graph = timers is None and steps >= 8 and self._graph_ok()
         self.particle_diag()
-        self._solve(dt)
-        self.record(0)
+        self._solve(dt, record_slot=0)
         i = 0
         if graph:
             # two eager steps warm every allocation / plan, then capture
@@ -263,8 +262,7 @@ class PifEngine:
         for k in range(i, steps):
             with dt.section("Gather"):
                 self.gather_push()
-            self._solve(dt)
-            self.record(k + 1)
+            self._solve(dt, record_slot=k + 1)
         if timers is not None:
             dt.flush(timers)
         return self.rec
@@ -298,7 +296,7 @@ class PifEngine:
         torch.cuda.current_stream(self.device).wait_stream(side)
         return g
 
-    def _solve(self, dt):
+    def _solve(self, dt, record_slot: int | None = None):
         with dt.section("Scatter"):
             self.deposit()
         if self.comm is not None:
@@ -306,6 +304,8 @@ class PifEngine:
                 self.allreduce()
         with dt.section("Gather"):
             self.solve_fields()
+            if record_slot is not None:   # W and the guard come out of this solve
+                self.record(record_slot)
 
     def step_once(self):
         """One full PD step (used by the bench loop and CUDA-graph capture)."""

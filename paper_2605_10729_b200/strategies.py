@@ -83,7 +83,10 @@ def records_from_table(table: np.ndarray, *, steps: int, dt: float, q: float, m:
     return out
 
 
-def _run_replicated(setup: RunSetup, comm: Comm | None, timers: Timers, device=None) -> dict:
+def _run_replicated(setup: RunSetup, comm: Comm | None, timers: Timers | None,
+                    device=None) -> dict:
+    """timers=None: no section timing, the steps replay from CUDA graphs;
+    a Timers: synchronised wall-clock sections (the reference's semantics)."""
     torch = require_cuda()
     spec = setup.spec
     plan = nufft.make_plan(spec.N, spec.L, setup.eps)
@@ -127,7 +130,7 @@ def _run_replicated(setup: RunSetup, comm: Comm | None, timers: Timers, device=N
         "initial": initial,
         "loop_seconds": loop_seconds,
         "steps": spec.steps,
-        "timers": timers,
+        "timers": timers if timers is not None else Timers(),
         "engine": eng,
     }
 
@@ -136,7 +139,7 @@ def run_serial(setup: RunSetup, ctx: RankContext, timers: Timers | None = None) 
     """Plain single-rank stepping (strategies.py:335-339): no communication."""
     if ctx.world_size != 1:
         raise ValueError("serial strategy runs on exactly one rank")
-    return _run_replicated(setup, None, timers or Timers(), ctx.device)
+    return _run_replicated(setup, None, timers, ctx.device)
 
 
 def run_particle_decomposition(setup: RunSetup, ctx: RankContext,
@@ -144,7 +147,7 @@ def run_particle_decomposition(setup: RunSetup, ctx: RankContext,
     """Particles split by id, modes replicated, allreduce-only communication
     (strategies.py:342-346)."""
     ctx.space = ctx.world
-    return _run_replicated(setup, ctx.world, timers or Timers(), ctx.device)
+    return _run_replicated(setup, ctx.world, timers, ctx.device)
 
 
 def run_domain_decomposition(setup: RunSetup, ctx: RankContext, timers=None) -> dict:

@@ -741,3 +741,29 @@ def test_smallest_grids_where_the_window_wraps_the_domain(N):
                           0.05, L)
     assert rel_max(st.ensemble.v, vo) <= 1e-12
     assert rel_max(st.ensemble.x, xo) <= 1e-12
+
+
+def test_landau_damping_rate_acceptance():
+    """The reference's acceptance criterion 6 (test_acceptance.py:219-231):
+    32^3 modes, 10 ppm, dt 0.05, 400 steps, serial; the fitted damping rate is
+    within 10% of the Landau dispersion root gamma = 0.1533 (k = 0.5)."""
+    spec = pb.landau_spec(N=32, ppm=10, dt=0.05, steps=400, seed=0)
+    res = pb.spawn_spmd(1, lambda ctx: pb.run_serial(pb.RunSetup(spec=spec, eps=1e-7), ctx))[0]
+    t = np.array([r.t for r in res["records"]])
+    w = np.array([r.field_energy for r in res["records"]])
+    gamma = pb.fit_damping_rate(t, w)
+    assert abs(gamma - 0.1533) <= 0.10 * 0.1533, gamma
+
+
+def test_serial_timer_coverage():
+    """test_strategies.py:412-425: Scatter + Gather cover >= 80% of the loop."""
+    from paper_2605_10729_b200.diag import Timers
+    setup = pb.RunSetup(spec=pb.landau_spec(N=16, ppm=10, dt=0.05, steps=10, seed=1))
+
+    def program(ctx):
+        tm = Timers()
+        return pb.run_serial(setup, ctx, tm), tm
+
+    result, tm = pb.spawn_spmd(1, program)[0]
+    hot = tm.inclusive["Scatter"] + tm.inclusive["Gather"]
+    assert hot >= 0.8 * result["loop_seconds"], (hot, result["loop_seconds"])
