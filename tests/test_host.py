@@ -250,3 +250,15 @@ def test_out_of_scope_strategies_raise():
         pb.run_domain_decomposition(None, None)
     with pytest.raises(NotImplementedError):
         pb.pic_step()
+
+
+def test_criterion_9_parameter_fidelity():
+    """test_acceptance.py:294-310: the benchmark specs' defaults."""
+    import numpy as np
+    lan = samplers.landau_spec()
+    assert lan.L == 4 * np.pi and lan.Q_e == -lan.L ** 3
+    assert (lan.k, lan.alpha, lan.dt, lan.steps) == (0.5, 0.05, 0.003125, 768)
+    pen = samplers.penning_spec()
+    assert (pen.L, pen.Q_e) == (25.0, -1562.5)
+    assert pen.B_ext == (0.0, 0.0, 5.0) and pen.stds == (2.0, 1.0, 3.0)
+    assert pen.e_kind == "quadrupole"
