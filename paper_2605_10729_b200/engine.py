@@ -165,7 +165,9 @@ class PifEngine:
         _native.call("pif_bin_perm", self.handle, self.parts.key.data_ptr(),
                      self.parts.rank.data_ptr(), self.count, self.parts.perm.data_ptr(),
                      self._stream())
-        self.launches += 3      # CUB scan (2 kernels) + perm
+        # cell scan (CUB: 2 kernels) + perm + work items (segment counts,
+        # CUB scan: 2, item table): 7 kernels (profiles/r03_launches.md)
+        self.launches += 7
 
     # -- stages -----------------------------------------------------------------
     def particle_diag(self):
@@ -184,7 +186,7 @@ class PifEngine:
     def modes(self):
         """cuFFT D2Z + truncate/deconvolve -> raw modes (head of the allreduce buffer)."""
         _native.call("pif_grid_to_modes", self.handle, self.raw.data_ptr(), self._stream())
-        self.launches += 1
+        self.launches += 1      # truncate/deconvolve; cuFFT D2Z (library) not counted
 
     def deposit(self):
         """Scatter stage: spread + modes."""
@@ -199,7 +201,7 @@ class PifEngine:
         """finish_deposit + Poisson + energy + guard + padded spectra + Z2D."""
         _native.call("pif_solve_fields", self.handle, self.raw.data_ptr(), self.shape,
                      self.rho.data_ptr(), self.scalars.data_ptr(), self._stream())
-        self.launches += 5      # poisson, energy, guard (2), pad; cuFFT Z2D not counted
+        self.launches += 5      # poisson, energy, guard (2), pad; cuFFT Z2D (library) not counted
 
     def interp_push(self):
         """Fused gather + Boris push + next cell keys + diagnostic sums: reads the
