@@ -232,6 +232,13 @@ class Comm:
             return values
         return np.array(res, copy=True)
 
+    def log_replayed_allreduce(self, values, times: int = 1):
+        """Record allreduces a CUDA-graph replay issued without passing through
+        allreduce_sum (the graph captured them once), so the CallLog keeps one
+        entry per executed collective."""
+        for _ in range(times):
+            self._t.job.log(self.rank, "allreduce", self.label, -1, _nbytes(values))
+
     def send(self, dest, payload):
         raise CommError("point-to-point send is outside the particle-decomposition path")
 

@@ -260,6 +260,8 @@ class PifEngine:
                 g = self._capture_pair(i + 1)
                 for _ in range(pairs):
                     g.replay()
+                    if self.comm is not None:   # the graph's two collectives
+                        self.comm.log_replayed_allreduce(self.red, 2)
                 i += 2 * pairs
         for k in range(i, steps):
             with dt.section("Gather"):
@@ -283,18 +285,27 @@ class PifEngine:
         side = torch.cuda.Stream(device=self.device)
         side.wait_stream(torch.cuda.current_stream(self.device))
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.stream(side):
-            with torch.cuda.graph(g, stream=side):
-                for _ in range(2):
-                    self.gather_push()
-                    self.deposit()
-                    self.allreduce()
-                    self.solve_fields()
-                    self._row[0, 0:1].copy_(self.scalars[0:1])
-                    self._row[0, 1:6].copy_(self.diag[0:5])
-                    self._row[0, 6:7].copy_(self.scalars[1:2])
-                    self.rec.index_copy_(0, self._slot, self._row)
-                    self._slot += 1
+        # capture records the collectives without running them: the call log
+        # gets its entries per replay instead (run())
+        log = self.comm.transport.job.call_log if self.comm is not None else None
+        if self.comm is not None:
+            self.comm.transport.job.call_log = None
+        try:
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(g, stream=side):
+                    for _ in range(2):
+                        self.gather_push()
+                        self.deposit()
+                        self.allreduce()
+                        self.solve_fields()
+                        self._row[0, 0:1].copy_(self.scalars[0:1])
+                        self._row[0, 1:6].copy_(self.diag[0:5])
+                        self._row[0, 6:7].copy_(self.scalars[1:2])
+                        self.rec.index_copy_(0, self._slot, self._row)
+                        self._slot += 1
+        finally:
+            if self.comm is not None:
+                self.comm.transport.job.call_log = log
         torch.cuda.current_stream(self.device).wait_stream(side)
         return g
 
