@@ -87,3 +87,26 @@ def test_no_unresolved_symbols_of_our_own():
     out = subprocess.run(["nm", "-D", "--undefined-only", _native.LIB_PATH], capture_output=True,
                          text=True, check=True).stdout
     assert "pif" not in out, out
+
+
+def test_product_path_fails_loudly_without_the_extension_or_a_gpu():
+    """No CPU fallback: a missing libpifb200.so raises on load, and the operator
+    API refuses to run without a CUDA device (this container has none)."""
+    import subprocess
+    import sys
+    code = ("import paper_2605_10729_b200._native as n\n"
+            "try:\n    n.load()\nexcept ImportError as e:\n    print('raised', 'no CPU fallback' in str(e))\n")
+    env = dict(os.environ, PIF_B200_LIB="/nonexistent/libpifb200.so")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         cwd=ROOT).stdout
+    assert "raised True" in out, out
+    import numpy as np
+    import pytest
+    import torch
+
+    import paper_2605_10729_b200 as pb
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    plan = pb.make_plan(8, 1.0, 1e-7)
+    with pytest.raises(RuntimeError, match="no CPU implementation"):
+        pb.type1(plan, np.zeros((4, 3)), np.ones(4))
