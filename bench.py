@@ -312,11 +312,15 @@ def run_b200(a):
     traffic = load_ncu_traffic()
     tr = traffic.get(f"interp_w{w}_ppg{per_gpu}")
     roofline = {
-        "bound": "fp64", "kernel": "interp_fast_kernel<8,true> (fused gather + Boris push)",
+        "bound": "tensor", "pipe": "fp64: DMMA (mma.sync m8n8k4 f64 tensor cores) and DFMA "
+                                  "share one ~37 TF/s pipe on B200",
+        "kernel": (f"interp_mma_kernel<{w}, 1>" if w <= 8 else f"interp_ring_kernel<{w}, 1>")
+                  + " (fused gather + Boris push)",
         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
         "traffic": tr,
-        "peak_source": "FP64 DFMA probe measured live in this run (MEASURED_PEAKS.json has no "
-                       "FP64 figure); HBM peak from MEASURED_PEAKS.json",
+        "peak_source": "fp64 peak measured live in this run by the DFMA probe (pif_probe_fp64; "
+                       "DMMA measured equal, profiles/r01_dmma_probe.txt); MEASURED_PEAKS.json "
+                       "has HBM and bf16 only; HBM peak from MEASURED_PEAKS.json",
         "algorithmic_flops_per_particle": {"interp": f_interp, "spread": f_spread,
                                            "step": f_step},
         "spread": {"achieved": per_gpu * f_spread / s_spr / 1e12,
