@@ -73,7 +73,7 @@ def test_interior_weight_polynomials_are_accurate():
 
     from paper_2605_10729_b200 import _native
     lib = _native.load()
-    for w in range(2, 9):
+    for w in range(2, 15):            # DMMA kernels (w <= 8) and ring kernels (9..14)
         err = (ctypes.c_double * 3)()
         mask = ctypes.c_int()
         _native.check(lib.pif_es_poly_info(w, 2.30 * w, err, ctypes.byref(mask)))
