@@ -44,7 +44,7 @@ struct Plan {
     double L = 0, eps = 0, beta = 0, h = 0, inv_L3 = 0, half_L3 = 0;
     int64_t n3 = 0, nhalf = 0;     // n^3, n*n*(n/2+1)
     int seg = 8;                   // cells per z-segment work item (set per binning)
-    int seg_target = 512;          // particles per work item the segment length aims at
+    int seg_target = 1024;         // particles per work item the segment length aims at
     double density = 0.0;          // particles per stencil cell at the last binning
     double *ring_scratch = nullptr;  // E per position for the wide-window gather
     bool wcache_on = false;        // spread keeps its window weights for the next gather
