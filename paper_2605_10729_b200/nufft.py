@@ -298,7 +298,7 @@ def gather3_real(plan: NufftPlan, components, points):
 
 
 # ---------------------------------------------------------------------------
-# direct-sum oracles of the reference API (nufft.py:199-231), on the GPU
+# direct-sum transforms of the reference API (nufft.py:199-231), computed on the GPU
 # ---------------------------------------------------------------------------
 
 _DIRECT_CHUNK = 2048
