@@ -1,9 +1,11 @@
 // Particle-side kernels of the PD-PIF step on sm_100a:
-//   binning (ES-stencil cell keys, counting-sort scatter),
+//   binning (ES-stencil cell keys, cell-order permutation, work items),
 //   type-1 spreading (replaces _kernels.spread_r, _kernels.py:57-96),
 //   type-2 gather fused with the Boris push (replaces _kernels.interp_r3,
 //   _kernels.py:125-183, and pif.boris_push, pif.py:140-158),
-//   diagnostics sums (strategies.py:96-106), generic wide-window fallbacks.
+//   diagnostics sums (strategies.py:96-106), FMA "ring" kernels for wide
+//   windows (w = 9..14), one-thread-per-particle kernels for the rest, the
+//   complex-strength variants and the host-layout (AoS) load / id-order output.
 //
 // Fast kernels (w <= 8): particles are binned by their ES-stencil start cell
 // (i0x, i0y, i0z), so every particle of a cell shares one w^3 footprint.  One
