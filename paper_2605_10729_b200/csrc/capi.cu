@@ -175,7 +175,7 @@ int pif_plan_create(const pif_plan_desc_t *d, int device, pif_plan_t *out) {
     if (d->N < 4 || d->N % 2) return pif::bad("N must be even and >= 4");
     if (!(d->L > 0) || !std::isfinite(d->L)) return pif::bad("invalid L");
     if (d->w < 2 || d->w > pif::kMaxW) return pif::bad("window width out of range");
-    if (d->n_up < d->N || d->n_up % 2 || d->n_up < d->w) return pif::bad("invalid n_up");
+    if (d->n_up < d->N || d->n_up % 2) return pif::bad("invalid n_up");   // w may exceed n_up
     if ((int64_t)d->n_up * d->n_up * d->n_up >= (int64_t)INT32_MAX)
         return pif::bad("fine grid too large for 32-bit cell keys");
     if (!d->deconv || !d->kvec || !d->shape_cic) return pif::bad("missing host tables");
