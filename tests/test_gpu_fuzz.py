@@ -18,8 +18,8 @@ TIGHT = 1e-12
 
 def _case(seed):
     rng = np.random.default_rng(1000 + seed)
-    N = int(rng.choice([4, 6, 8, 10, 12, 16]))
-    eps = float(rng.choice([1e-3, 1e-5, 1e-7, 1e-9, 1e-12, 1e-14]))
+    N = int(rng.choice([4, 6, 8, 10, 12, 16, 24]))
+    eps = float(rng.choice([1e-1, 1e-2, 1e-3, 1e-5, 1e-7, 1e-9, 1e-12, 1e-14, 1e-15, 1e-16]))
     M = int(rng.integers(1, 20000))
     L = float(rng.choice([1.0, 2 * np.pi, 25.0]))
     if rng.random() < 0.5:
@@ -70,3 +70,20 @@ def test_random_engine_step_matches_oracle(seed):
     assert rel_max(st.ensemble.v, vo) <= 1e-11, (N, eps, M)
     dx = np.abs(st.ensemble.x - xo)
     assert np.max(np.minimum(dx, L - dx)) <= 1e-11 * L, (N, eps, M)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_pd_run_matches_serial(seed):
+    """PD over 1-3 thread ranks equals the serial run on random small specs."""
+    rng = np.random.default_rng(2000 + seed)
+    mk = pb.landau_spec if rng.random() < 0.5 else pb.penning_spec
+    spec = mk(N=int(rng.choice([4, 8, 12])), ppm=int(rng.integers(1, 6)),
+              dt=float(rng.choice([0.003125, 0.05])), steps=int(rng.integers(1, 12)),
+              seed=int(rng.integers(0, 5)))
+    setup = pb.RunSetup(spec=spec, eps=float(rng.choice([1e-5, 1e-7, 1e-10])))
+    ref = pb.spawn_spmd(1, lambda ctx: pb.run_serial(setup, ctx))[0]
+    ranks = int(rng.integers(2, 4))
+    got = pb.spawn_spmd(ranks, lambda ctx: pb.run_particle_decomposition(setup, ctx))[0]
+    a = np.array([r.total_energy for r in ref["records"]])
+    b = np.array([r.total_energy for r in got["records"]])
+    assert np.max(np.abs(a - b) / np.abs(a)) <= 1e-10
