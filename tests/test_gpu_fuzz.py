@@ -87,3 +87,23 @@ def test_random_pd_run_matches_serial(seed):
     a = np.array([r.total_energy for r in ref["records"]])
     b = np.array([r.total_energy for r in got["records"]])
     assert np.max(np.abs(a - b) / np.abs(a)) <= 1e-10
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_device_sampler_matches_host(seed):
+    """The device Philox samplers regenerate the host (reference) ensemble for
+    random specs, seeds and id slices."""
+    from paper_2605_10729_b200.samplers import sample_benchmark, sample_device
+    rng = np.random.default_rng(3000 + seed)
+    mk = pb.landau_spec if rng.random() < 0.5 else pb.penning_spec
+    spec = mk(N=int(rng.choice([4, 8, 12])), ppm=int(rng.integers(1, 30)),
+              seed=int(rng.integers(0, 1000)))
+    n = spec.num_particles
+    lo = int(rng.integers(0, n))
+    hi = int(rng.integers(lo, n + 1))
+    host = sample_benchmark(spec, spec.seed, (lo, hi))
+    x, v, ids = sample_device(spec, (lo, hi), "cuda")
+    assert np.array_equal(ids.cpu().numpy(), host.ids)
+    if hi > lo:
+        assert np.max(np.abs(x.cpu().numpy() - host.x)) <= 1e-10 * spec.L
+        assert np.max(np.abs(v.cpu().numpy() - host.v)) <= 1e-12
