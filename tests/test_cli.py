@@ -142,3 +142,38 @@ def test_run_refuses_existing_outputs(tmp_path, cuda):
     assert main(argv) == EXIT_OK
     assert main(argv) == EXIT_RUNTIME
     assert main(argv + ["--overwrite"]) == EXIT_OK
+
+
+def test_config_file_round_trip_property(tmp_path):
+    """Any valid configuration written as key=value lines or JSON parses back to
+    the same RunConfig (hypothesis)."""
+    from hypothesis import given, settings
+    from hypothesis import strategies as st
+
+    cfgs = st.fixed_dictionaries({
+        "benchmark": st.sampled_from(["landau", "penning"]),
+        "strategy": st.sampled_from(["serial", "pd"]),
+        "modes": st.integers(2, 40).map(lambda k: 2 * k),
+        "ppm": st.integers(1, 64),
+        "dt": st.floats(1e-4, 1.0),
+        "steps": st.integers(1, 1000),
+        "eps_fine": st.sampled_from([1e-3, 1e-7, 1e-12]),
+        "shape": st.sampled_from(["delta", "cic"]),
+        "seed": st.integers(0, 2 ** 31),
+        "log_comm": st.booleans(),
+    })
+
+    @settings(max_examples=60, deadline=None)
+    @given(cfgs, st.booleans())
+    def check(d, as_json):
+        path = tmp_path / ("c.json" if as_json else "c.txt")
+        if as_json:
+            path.write_text(json.dumps(d))
+        else:
+            path.write_text("\n".join(f"{k} = {v!r}" if isinstance(v, float) else f"{k}={v}"
+                                      for k, v in d.items()))
+        cfg = cli.build_config(cli.make_parser().parse_args(["--config", str(path)]))
+        for k, v in d.items():
+            assert getattr(cfg, k) == v, (k, getattr(cfg, k), v)
+
+    check()
