@@ -46,8 +46,11 @@ def parse():
     ap.add_argument("--eps", type=float, default=1e-7)
     ap.add_argument("--dt", type=float, default=0.003125)
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
-    ap.add_argument("--cpu-particles", type=int, default=1 << 20)
+    ap.add_argument("--cpu-particles", type=int, default=1 << 24,
+                    help="particles in the CPU (reference-algorithm) sample")
     ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--cpu-max-steps", type=int, default=8,
+                    help="cap on the reference arm's timed steps (bounded run time)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None,
@@ -137,8 +140,12 @@ class ClockSampler:
 # CPU baseline / reference arm (oracle port of the reference algorithm)
 # ---------------------------------------------------------------------------
 
-def cpu_reference_run(a, particles: int, steps: int, warmup: int):
-    """Oracle PD on all host cores: returns (particle-steps/s, cores, sample text)."""
+def cpu_reference_run(a, particles: int, steps: int, warmup: int, full_particles: int):
+    """Oracle PD on all host cores (one rank thread per core, like the
+    reference's spawn_spmd PD run).  Returns a dict: measured particle-steps/s
+    at `particles`, the per-step phase split, and the explicit extrapolation to
+    `full_particles` (particle phases scale with the count, the mode-space
+    FFT phases do not)."""
     import numpy as np  # noqa: F401
     from oracle import pif_oracle as o
     from paper_2605_10729_b200.samplers import landau_spec, penning_spec, sample_benchmark
@@ -152,14 +159,31 @@ def cpu_reference_run(a, particles: int, steps: int, warmup: int):
                   B=spec.B_ext, e_kind=spec.e_kind, dt=a.dt, ranks=cores)
     for _ in range(warmup):
         run.step()
+    run.phase_s = dict.fromkeys(run.PHASES, 0.0)
     t0 = time.perf_counter()
     for _ in range(steps):
         run.step()
-    dt = time.perf_counter() - t0
+    sec = (time.perf_counter() - t0) / steps
     M = ens.count
-    sample = (f"{M} particles ({ppm}/mode) of the same {a.N}^3 workload, {steps} PD steps on "
-              f"{cores} host threads (oracle port: C window kernels + numpy pocketfft)")
-    return M * steps / dt, cores, sample, dt / steps
+    split = {k: v / steps for k, v in run.phase_s.items()}
+    linear = split["spread"] + split["interp"] + split["push"]
+    fixed = split["fftn"] + split["field_grids"]
+    other = max(0.0, sec - linear - fixed)          # Poisson, energy, tree sum (fixed)
+    scale = full_particles / M
+    t_full = linear * scale + fixed + other
+    sample = (f"{M} particles ({ppm}/mode) of the same {a.N}^3 workload (eps {a.eps:g}), "
+              f"{steps} PD steps on {cores} host threads (oracle port of the reference "
+              "algorithm: C window kernels + numpy pocketfft; one rank slice per thread)")
+    return {
+        "value": M / sec, "cores": cores, "sample": sample, "sec_per_step": sec,
+        "particles_timed": M, "steps_timed": steps,
+        "split_s_per_step": {**{k: round(v, 6) for k, v in split.items()},
+                             "other": round(other, 6)},
+        "extrapolated": {"particles": full_particles, "value": full_particles / t_full,
+                         "sec_per_step": t_full,
+                         "how": "particle phases (spread, interp, push) x particles ratio + "
+                                "fixed mode-space phases (fftn, 3x ifftn, Poisson, sums)"},
+    }
 
 
 def run_reference(a):
@@ -167,18 +191,24 @@ def run_reference(a):
     if rank != 0:
         return
     cfg, w, per_gpu, glob = workload_config(a, world)
-    # K timed steps after W warm-ups, each a bounded sample (cpu_particles) of the
-    # workload; capped so a long GPU-side K still ends within a couple of minutes
-    steps = max(1, min(a.steps, 30))
-    warm = max(0, min(a.warmup, 3))
-    val, cores, sample, sec = cpu_reference_run(a, a.cpu_particles, steps, warm)
+    # K timed steps after W warm-ups, each one PD step over a bounded sample
+    # (cpu_particles) of the workload; capped so the arm ends within minutes
+    steps = max(1, min(a.steps, a.cpu_max_steps))
+    warm = max(0, min(a.warmup, 1))
+    r = cpu_reference_run(a, a.cpu_particles, steps, warm, glob)
+    val = r["value"]
+    cfg = dict(cfg)
+    cfg["workload_timed"] = (f"{r['particles_timed']} particles per step (bounded CPU sample "
+                             f"of the {glob}-particle workload)")
+    cfg["particles_timed"] = r["particles_timed"]
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
-        "steps": steps, "warmup": warm, "ms_per_step": sec * 1e3,
+        "steps": steps, "warmup": warm, "ms_per_step": r["sec_per_step"] * 1e3,
         "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference samplers, seed 0)", "config": cfg,
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": sample},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": r["cores"], "kind": "port",
+                         "sample": r["sample"], "split_s_per_step": r["split_s_per_step"],
+                         "extrapolated_full_size": r["extrapolated"]},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -264,6 +294,7 @@ def run_b200(a):
     t_bin = [(ev(), ev()) for _ in range(K)]
     t_fld = [(ev(), ev()) for _ in range(K)]
     t_red = [(ev(), ev()) for _ in range(K)]
+    t_mod = [(ev(), ev()) for _ in range(K)]
     start, stop = ev(), ev()
     clocks = ClockSampler(dev.index)
     if rank == 0:
@@ -273,6 +304,7 @@ def run_b200(a):
     if world > 1:
         dist.barrier()
     launches0 = eng.launches
+    eng.fft_timing(K)
     start.record()
     for i in range(K):
         t_int[i][0].record()
@@ -284,7 +316,9 @@ def run_b200(a):
         t_spr[i][0].record()
         eng.spread()
         t_spr[i][1].record()
+        t_mod[i][0].record()
         eng.modes()
+        t_mod[i][1].record()
         t_red[i][0].record()
         eng.allreduce()
         t_red[i][1].record()
@@ -297,6 +331,8 @@ def run_b200(a):
         dist.barrier()
     clk = clocks.stop() if rank == 0 else None
     launches = eng.launches - launches0
+    d2z_ms, z2d_ms = eng.fft_times()
+    eng.fft_timing(0)
     T = start.elapsed_time(stop) * 1e-3
     if world > 1:
         tt = torch.tensor([T], dtype=torch.float64, device=dev)
@@ -304,6 +340,7 @@ def run_b200(a):
         T = float(tt[0])
     avg = lambda ts: sum(a_.elapsed_time(b_) for a_, b_ in ts) / len(ts) * 1e-3  # noqa: E731
     s_int, s_spr, s_bin, s_fld, s_red = avg(t_int), avg(t_spr), avg(t_bin), avg(t_fld), avg(t_red)
+    s_mod = avg(t_mod)
     value = glob * K / T
     f_interp = 6 * w ** 3 + w ** 2
     f_spread = 2 * w ** 3 + w ** 2
@@ -328,7 +365,14 @@ def run_b200(a):
         "step_fp64_frac": (per_gpu * f_step / (T / K) / 1e12) / peak,
         "hbm_frac_step": None,
         "stage_ms": {"interp_push": s_int * 1e3, "bin": s_bin * 1e3, "spread": s_spr * 1e3,
-                     "fields": s_fld * 1e3, "allreduce": s_red * 1e3},
+                     "modes": s_mod * 1e3, "d2z": d2z_ms, "truncate": s_mod * 1e3 - (d2z_ms or 0.0),
+                     "allreduce": s_red * 1e3, "fields": s_fld * 1e3, "z2d": z2d_ms,
+                     "poisson_guard_pad": s_fld * 1e3 - (z2d_ms or 0.0)},
+        "stage_notes": "CUDA events on the launching stream, averaged over the K timed steps; "
+                       "d2z / z2d are the cuFFT execs alone (native event pairs around "
+                       "cufftExecD2Z / cufftExecZ2D, pif_fft_timing); modes = d2z + truncate/"
+                       "deconvolve kernel; fields = finish_deposit+Poisson+energy+guard+pad "
+                       "kernels + z2d",
     }
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -344,8 +388,11 @@ def run_b200(a):
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        val, cores, sample, _ = cpu_reference_run(a, a.cpu_particles, a.cpu_steps, 0)
-        cpu = {"value": val, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+        r = cpu_reference_run(a, a.cpu_particles, a.cpu_steps, 0, glob)
+        cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "port",
+               "sample": r["sample"], "particles_timed": r["particles_timed"],
+               "split_s_per_step": r["split_s_per_step"],
+               "extrapolated_full_size": r["extrapolated"]}
 
     if rank == 0:
         line = {

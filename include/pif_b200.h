@@ -221,6 +221,16 @@ int pif_type2_complex(pif_plan_t plan, const double *modes, const double *pts, i
  * iterations of 8 independent FMAs; *flops_out = flops issued. */
 int pif_probe_fp64(double *scratch, int blocks, int threads, int iters, void *stream,
                    double *flops_out);
+/* cuFFT stage timing (the north star's "cuFFT call timed separately";
+ * the reference times its fftn/ifftn inside Scatter/Gather, strategies.py:158-170).
+ * pif_fft_timing(plan, slots): record CUDA events around each of the next
+ * `slots` D2Z execs (pif_grid_to_modes) and Z2D execs (pif_solve_fields /
+ * pif_fields_from_modes, incl. the interleave when the strided C2R is absent);
+ * 0 disables.  Never records inside a stream capture.
+ * pif_fft_times: waits for the recorded events, returns the summed milliseconds
+ * and counts since the last call, and restarts the rings. */
+int pif_fft_timing(pif_plan_t plan, int slots);
+int pif_fft_times(pif_plan_t plan, double *d2z_ms, double *z2d_ms, int *n_d2z, int *n_z2d);
 /* ---- device samplers (reference bench.py:67-122) -----
  * One numpy Philox4x64-10 stream per (seed, attribute): counter[4] / key[2] as
  * numpy's Philox(SeedSequence((seed, attr))).state holds them; uint64 number j

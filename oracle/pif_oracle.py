@@ -22,6 +22,7 @@ import math
 import os
 import subprocess
 import threading
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -460,7 +461,14 @@ def run_pd(plan: Plan, x: np.ndarray, v: np.ndarray, q: float, m: float, *, L: f
 class PDRun:
     """Stateful oracle PD stepper for timing (bench.py cpu_baseline and
     --impl reference): `ranks` id slices on `ranks` threads, like the
-    reference's spawn_spmd PD run (strategies.py:285-303)."""
+    reference's spawn_spmd PD run (strategies.py:285-303).
+
+    ``phase_s`` accumulates wall seconds per phase so the bench can report the
+    split between the particle kernels (spread, interp, push: linear in the
+    particle count) and the mode-space work (per-rank fftn + truncate, 3 x
+    ifftn of the padded spectra: fixed per step for a given N)."""
+
+    PHASES = ("spread", "fftn", "field_grids", "interp", "push")
 
     def __init__(self, plan: Plan, x, v, q, m, *, L, B=(0.0, 0.0, 0.0), e_kind="none", dt,
                  ranks=1, shape="delta"):
@@ -474,6 +482,7 @@ class PDRun:
             hi = lo + base + (1 if r < extra else 0)
             self.xs.append(np.ascontiguousarray(x[lo:hi]))
             self.vs.append(np.ascontiguousarray(v[lo:hi]))
+        self.phase_s = dict.fromkeys(self.PHASES, 0.0)
         self.rho = self._solve()
 
     def _par(self, fn):
@@ -486,10 +495,20 @@ class PDRun:
             t.join()
         return out
 
+    def _timed(self, phase, fn):
+        t0 = time.perf_counter()
+        out = fn()
+        self.phase_s[phase] += time.perf_counter() - t0
+        return out
+
     def _solve(self):
-        raws = self._par(lambda r: type1(self.plan, self.xs[r],
-                                         np.full(self.xs[r].shape[0], self.q)))
-        return finish_deposit(tree_sum(raws), self.plan, self.shape)
+        # type1 per rank (nufft.py:122-145), split into its spread and its
+        # fftn + truncate so the two can be timed apart
+        plan = self.plan
+        grids = self._timed("spread", lambda: self._par(lambda r: spread_real(
+            plan, prep_points(self.xs[r], self.L), np.full(self.xs[r].shape[0], self.q))))
+        raws = self._timed("fftn", lambda: self._par(lambda r: modes_from_grid(plan, grids[r])))
+        return finish_deposit(tree_sum(raws), plan, self.shape)
 
     def step(self):
         plan = self.plan
@@ -500,10 +519,14 @@ class PDRun:
             c = f.copy()
             apply_shape(c, s)
             comps.append(c)
-        grids = field_grids(plan, comps)
-        E_at = self._par(lambda r: interp3(plan, grids, prep_points(self.xs[r], self.L)))
-        for r in range(self.ranks):
-            self.xs[r], self.vs[r] = boris_push(self.xs[r], self.vs[r], E_at[r], self.q, self.m,
-                                                self.B, self.e_kind, self.dt, self.L)
+        grids = self._timed("field_grids", lambda: field_grids(plan, comps))
+        E_at = self._timed("interp", lambda: self._par(
+            lambda r: interp3(plan, grids, prep_points(self.xs[r], self.L))))
+
+        def push():
+            for r in range(self.ranks):
+                self.xs[r], self.vs[r] = boris_push(self.xs[r], self.vs[r], E_at[r], self.q,
+                                                    self.m, self.B, self.e_kind, self.dt, self.L)
+        self._timed("push", push)
         self.rho = self._solve()
         return field_energy(poisson_efield(self.rho, self.L), self.L)

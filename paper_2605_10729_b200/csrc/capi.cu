@@ -59,6 +59,12 @@ void release(Plan &p) {
         if (q) cudaFree(q);
     if (p.d2z) cufftDestroy(p.d2z);
     if (p.z2d3) cufftDestroy(p.z2d3);
+    if (p.fft_ev) {
+        for (int i = 0; i < 4 * p.fft_slots; ++i) cudaEventDestroy(p.fft_ev[i]);
+        delete[] p.fft_ev;
+        p.fft_ev = nullptr;
+        p.fft_slots = 0;
+    }
     if (p.z2z) cufftDestroy(p.z2z);
 }
 
@@ -386,6 +392,60 @@ int pif_interp_push_perm(pif_plan_t plan, const pif_soa_t *src, const int32_t *p
                                 rank, diag, nullptr, s);
     dst->count = d.count;
     return rc;
+}
+
+
+int pif_fft_timing(pif_plan_t plan, int slots) {
+    if (!plan) return pif::bad("null plan");
+    if (slots < 0 || slots > 1 << 16) return pif::bad("slots out of range");
+    Plan &p = plan->p;
+    pif::DeviceGuard g(p.device);
+    if (p.fft_ev) {
+        cudaDeviceSynchronize();
+        for (int i = 0; i < 4 * p.fft_slots; ++i) cudaEventDestroy(p.fft_ev[i]);
+        delete[] p.fft_ev;
+        p.fft_ev = nullptr;
+    }
+    p.fft_slots = p.fft_nd = p.fft_nz = 0;
+    if (!slots) return PIF_OK;
+    p.fft_ev = new (std::nothrow) cudaEvent_t[4 * slots];
+    if (!p.fft_ev) return pif::bad("out of host memory");
+    for (int i = 0; i < 4 * slots; ++i) {
+        cudaError_t e = cudaEventCreate(&p.fft_ev[i]);
+        if (e != cudaSuccess) {
+            for (int j = 0; j < i; ++j) cudaEventDestroy(p.fft_ev[j]);
+            delete[] p.fft_ev;
+            p.fft_ev = nullptr;
+            return pif::fail_cuda(e, "cudaEventCreate");
+        }
+    }
+    p.fft_slots = slots;
+    return PIF_OK;
+}
+
+int pif_fft_times(pif_plan_t plan, double *d2z_ms, double *z2d_ms, int *n_d2z, int *n_z2d) {
+    if (!plan || !d2z_ms || !z2d_ms || !n_d2z || !n_z2d) return pif::bad("null argument");
+    Plan &p = plan->p;
+    pif::DeviceGuard g(p.device);
+    double sums[2] = {0.0, 0.0};
+    const int counts[2] = {p.fft_nd, p.fft_nz};
+    for (int which = 0; which < 2; ++which) {
+        for (int k = 0; k < counts[which]; ++k) {
+            cudaEvent_t a = p.fft_ev[which * 2 * p.fft_slots + 2 * k];
+            cudaEvent_t b = p.fft_ev[which * 2 * p.fft_slots + 2 * k + 1];
+            float ms = 0.f;
+            cudaError_t e = cudaEventSynchronize(b);
+            if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, a, b);
+            if (e != cudaSuccess) return pif::fail_cuda(e, "cudaEventElapsedTime");
+            sums[which] += ms;
+        }
+    }
+    *d2z_ms = sums[0];
+    *z2d_ms = sums[1];
+    *n_d2z = counts[0];
+    *n_z2d = counts[1];
+    p.fft_nd = p.fft_nz = 0;
+    return PIF_OK;
 }
 
 int pif_grid_to_modes(pif_plan_t plan, double *modes, void *stream) {

@@ -253,6 +253,7 @@ int blocks_for(int64_t work, int threads, int sm_count, int cap_per_sm = 16) {
 int exec_z2d_fields(Plan &p, cudaStream_t s) {
     cufftResult r = cufftSetStream(p.z2d3, s);
     if (r != CUFFT_SUCCESS) return fail_cufft(r, "cufftSetStream(z2d)");
+    fft_mark(p, true, false, s);
     if (p.z2d_strided) {
         r = cufftExecZ2D(p.z2d3, reinterpret_cast<cufftDoubleComplex *>(p.spec), p.field);
         if (r != CUFFT_SUCCESS) return fail_cufft(r, "cufftExecZ2D");
@@ -264,6 +265,7 @@ int exec_z2d_fields(Plan &p, cudaStream_t s) {
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return fail_cuda(e, "interleave_kernel");
     }
+    fft_mark(p, true, true, s);
     p.field_valid = true;
     return PIF_OK;
 }
@@ -285,11 +287,23 @@ int guard_and_pad(Plan &p, const double2 *ex, const double2 *ey, const double2 *
 
 }  // namespace
 
+void fft_mark(Plan &p, bool z2d, bool end, cudaStream_t s) {
+    if (!p.fft_slots) return;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+    int &k = z2d ? p.fft_nz : p.fft_nd;
+    if (k >= p.fft_slots) return;                  // ring full: later execs are not timed
+    cudaEventRecord(p.fft_ev[(z2d ? 2 * p.fft_slots : 0) + 2 * k + (end ? 1 : 0)], s);
+    if (end) ++k;
+}
+
 int launch_modes_from_spec(Plan &p, double *modes, cudaStream_t s) {
     cufftResult r = cufftSetStream(p.d2z, s);
     if (r != CUFFT_SUCCESS) return fail_cufft(r, "cufftSetStream(d2z)");
+    fft_mark(p, false, false, s);
     r = cufftExecD2Z(p.d2z, p.grid, reinterpret_cast<cufftDoubleComplex *>(p.spec));
     if (r != CUFFT_SUCCESS) return fail_cufft(r, "cufftExecD2Z");
+    fft_mark(p, false, true, s);
     const int64_t N3 = (int64_t)p.N * p.N * p.N;
     modes_from_spec_kernel<<<blocks_for(N3, 256, p.sm_count), 256, 0, s>>>(
         p.spec, p.deconv, reinterpret_cast<double2 *>(modes), p.N, p.n, 1.0 / (double)p.n3);

@@ -89,6 +89,10 @@ struct Plan {
     bool force_ring = false;       // PIF_FORCE_RING: w = 8 through the ring kernels (A/B)     // env PIF_FORCE_GENERIC=1: one-thread-per-particle kernels
     int sm_count = 148;
     int64_t bytes = 0;
+    // optional cuFFT timing (bench.py): event pairs around each D2Z / Z2D exec,
+    // slot k of each ring holds the k-th exec since the last pif_fft_times
+    cudaEvent_t *fft_ev = nullptr;  // [d2z begin, d2z end] x slots, then z2d pairs
+    int fft_slots = 0, fft_nd = 0, fft_nz = 0;
     EsPolyHost poly{};              // interior weight polynomials for w <= 8
     double poly_err = 0;            // their max abs error (checked at creation)
 };
@@ -96,6 +100,9 @@ struct Plan {
 void set_error(const std::string &msg);
 int fail_cuda(cudaError_t e, const char *where);
 int fail_cufft(cufftResult r, const char *where);
+// record the begin (end=false) / end event of a cuFFT exec into the timing ring
+// (no-op unless pif_fft_timing enabled it, and never inside a graph capture)
+void fft_mark(Plan &p, bool z2d, bool end, cudaStream_t s);
 
 // Kernel launchers (defined in the .cu files); all return PIF_* codes.
 int launch_wrap(Plan &p, double *x, double *y, double *z, int64_t M, cudaStream_t s);

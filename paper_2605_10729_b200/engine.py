@@ -40,7 +40,6 @@ class PifEngine:
     def __init__(self, plan, count: int, device, *, q: float, m: float, externals, dt: float,
                  shape: str = "delta", comm=None):
         torch = require_cuda()
-        from .pif import boris_constants
         if shape not in _native.SHAPE:
             raise ValueError(f"unknown shape {shape!r}")
         if dt <= 0:
@@ -64,6 +63,23 @@ class PifEngine:
         self.diag = self.red[2 * N3:2 * N3 + 6]
         self.rho = torch.zeros((plan.N,) * 3, dtype=torch.complex128, device=self.device)
         self.scalars = torch.zeros(4, **f64)
+        self.configure(q=q, m=m, externals=externals, dt=dt, shape=shape)
+        self.comm = comm
+        self.rec = None
+        self.dtimers = DeviceTimers(enabled=False)
+        self.launches = 0   # native kernel launches issued (for bench accounting)
+        self.weight_cache = self._enable_weight_cache()
+
+    def configure(self, *, q: float, m: float, externals, dt: float, shape: str = "delta"):
+        """(Re)set the per-run constants: charge/mass per particle, the Boris
+        constants exactly as numpy forms them (pif.py:146-153), the external
+        field kind and the particle shape.  Cheap; lets a cached engine serve
+        successive pif_step calls."""
+        from .pif import boris_constants
+        if shape not in _native.SHAPE:
+            raise ValueError(f"unknown shape {shape!r}")
+        if dt <= 0:
+            raise ValueError(f"dt must be positive, got {dt}")
         self.q, self.m, self.dt = float(q), float(m), float(dt)
         half, tq, sq, has_b = boris_constants(self.q / self.m, self.dt, externals.B)
         self.half = float(half)
@@ -72,11 +88,31 @@ class PifEngine:
         self.e_kind = _native.EXT[externals.e_kind]
         self.shape = _native.SHAPE[shape]
         self.externals = externals
-        self.comm = comm
-        self.rec = None
-        self.dtimers = DeviceTimers(enabled=False)
-        self.launches = 0   # native kernel launches issued (for bench accounting)
-        self.weight_cache = self._enable_weight_cache()
+        return self
+
+    @classmethod
+    def cached(cls, plan, count: int, device, *, q: float, m: float, externals, dt: float,
+               shape: str = "delta"):
+        """The engine a plan keeps for `count` particles on `device`, created on
+        first use and reconfigured on every later call (no new cuFFT plans,
+        grids or particle store per call).  Used by the reference-shaped
+        single-rank API (pif_step, B200FieldOps): not for concurrent use."""
+        torch = require_cuda()
+        dev = torch.device(device)
+        idx = dev.index if dev.index is not None else torch.cuda.current_device()
+        key = (idx, int(count))
+        with plan._lock:
+            cache = plan.__dict__.setdefault("_engines", {})
+            eng = cache.get(key)
+        if eng is None:
+            eng = cls(plan, count, torch.device("cuda", idx), q=q, m=m, externals=externals,
+                      dt=dt, shape=shape)
+            eng.created_by_cache = True
+            with plan._lock:
+                cache[key] = eng
+            return eng
+        eng.created_by_cache = False
+        return eng.configure(q=q, m=m, externals=externals, dt=dt, shape=shape)
 
     def _enable_weight_cache(self) -> bool:
         """PIF_WEIGHT_CACHE=1: the spread keeps its window weights for the next
@@ -111,15 +147,20 @@ class PifEngine:
         eng.load(ens.x, ens.v, np.arange(ens.count, dtype=np.int64))
         return eng
 
-    def load(self, x, v, ids):
-        """Upload an AoS ensemble and bin it into cell order."""
+    def load(self, x, v=None, ids=None):
+        """Upload an AoS ensemble and bin it into cell order (v=None: positions
+        only, for operators that never push)."""
         torch = require_cuda()
         if not is_torch(x):
             x = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64))
+        if v is not None and not is_torch(v):
             v = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64))
-        if not is_torch(ids):
+        if ids is None:
+            ids = torch.arange(self.count, dtype=torch.int64, device=self.device)
+        elif not is_torch(ids):
             ids = torch.from_numpy(np.ascontiguousarray(ids, dtype=np.int64))
-        self.parts.upload(x.to(self.device), v.to(self.device), ids.to(self.device))
+        self.parts.upload(x.to(self.device), None if v is None else v.to(self.device),
+                          ids.to(self.device))
         if self.count:
             s = self._stream()
             cur = self._soa()
@@ -187,6 +228,20 @@ class PifEngine:
         """cuFFT D2Z + truncate/deconvolve -> raw modes (head of the allreduce buffer)."""
         _native.call("pif_grid_to_modes", self.handle, self.raw.data_ptr(), self._stream())
         self.launches += 1      # truncate/deconvolve; cuFFT D2Z (library) not counted
+
+    def fft_timing(self, slots: int):
+        """Time the next `slots` cuFFT D2Z / Z2D execs with native event pairs
+        (pif_fft_timing; 0 disables)."""
+        _native.call("pif_fft_timing", self.handle, int(slots))
+
+    def fft_times(self):
+        """(mean D2Z ms, mean Z2D ms) over the execs timed since the last call."""
+        d, z = ctypes.c_double(), ctypes.c_double()
+        nd, nz = ctypes.c_int(), ctypes.c_int()
+        _native.call("pif_fft_times", self.handle, ctypes.byref(d), ctypes.byref(z),
+                     ctypes.byref(nd), ctypes.byref(nz))
+        return (d.value / nd.value if nd.value else None,
+                z.value / nz.value if nz.value else None)
 
     def deposit(self):
         """Scatter stage: spread + modes."""

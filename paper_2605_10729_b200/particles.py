@@ -142,10 +142,13 @@ class DeviceParticles:
         import torch
         M = self.count
         xt = torch.as_tensor(x, dtype=torch.float64).reshape(M, 3)
-        vt = torch.as_tensor(v, dtype=torch.float64).reshape(M, 3)
         soa = self.buf[self.cur]
         soa[0:3, :M].copy_(xt.t(), non_blocking=True)
-        soa[3:6, :M].copy_(vt.t(), non_blocking=True)
+        if v is None:
+            soa[3:6, :M].zero_()
+        else:
+            vt = torch.as_tensor(v, dtype=torch.float64).reshape(M, 3)
+            soa[3:6, :M].copy_(vt.t(), non_blocking=True)
         self.ids[self.cur][:M].copy_(torch.as_tensor(ids, dtype=torch.int64), non_blocking=True)
 
     def download(self, sort_by_id: bool = True):

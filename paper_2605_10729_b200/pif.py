@@ -198,14 +198,25 @@ class StepState:
 def pif_step(state: StepState, timers=NULL_TIMERS) -> StepState:
     """One PIF cycle (pif.py:178-190): deposit, Poisson, gather, push — on the
     device through the fused engine (one spread, one field solve, one fused
-    interp+push launch)."""
+    interp+push launch).  The engine (native plan, cuFFT plans, grids, SoA
+    store) is created once per (plan, device, particle count) and reused by
+    later calls; raises FieldSymmetryError when the gathered field modes lost
+    their Hermitian pairing, as gather_efield does (pif.py:128-133)."""
+    from ._device import default_device
     from .engine import PifEngine
     ens = state.ensemble
-    eng = PifEngine.for_ensemble(ens, state.plan, state.externals, state.dt, state.shape)
+    eng = PifEngine.cached(state.plan, ens.count, default_device(ens.x), q=ens.q_per_particle,
+                           m=ens.m_per_particle, externals=state.externals, dt=state.dt,
+                           shape=state.shape)
     with timers.section("Scatter"):
+        eng.load(ens.x, ens.v)
         eng.deposit()
     with timers.section("Gather"):
         eng.solve_fields()
+        guard = float(eng.scalars[1])
+        if guard > 1e-10:
+            raise FieldSymmetryError(f"field modes lost Hermitian symmetry (relative mismatch "
+                                     f"{guard:.3e})")
     with timers.section("ParticleUpdate"):
         eng.gather_push()
     eng.store_into(ens)
