@@ -221,6 +221,33 @@ int pif_type2_complex(pif_plan_t plan, const double *modes, const double *pts, i
  * iterations of 8 independent FMAs; *flops_out = flops issued. */
 int pif_probe_fp64(double *scratch, int blocks, int threads, int iters, void *stream,
                    double *flops_out);
+/* ---- deterministic mode: the reference is bit-reproducible by construction
+ * (serial numba kernels _kernels.py:1-5, fixed-order tree sums comm.py:329-339;
+ * its tests test_strategies.py:57-62, 405-409 compare runs with array_equal).
+ * When enabled, binning is a stable sort of the cell keys (particles of a cell
+ * keep their buffer order instead of atomic arrival order) and the spread
+ * writes each work item's planes to its own buffer slice, summed per grid point
+ * in a fixed order (det_reduce_kernel) instead of REDG.ADD.F64.  The caller
+ * takes the step's diagnostic sums from pif_particle_diag (fixed-order) after
+ * the push.  Same results to rounding as the default mode, identical bits run
+ * to run.  Only for the DMMA kernels (w <= 8); PIF_ERR_VALUE otherwise. */
+int pif_set_deterministic(pif_plan_t plan, int enable);
+int pif_is_deterministic(pif_plan_t plan);
+
+/* ---- in-process communicators: replaces comm.allreduce_sum's fixed-order
+ * tree over rank threads (comm.py:329-339, 391-408) for spawn_spmd's thread
+ * ranks (comm.py:483-528), one GPU per rank.
+ * pif_comm_init_all: ncclCommInitAll over `devices` (distinct; one rank per
+ * device), comms_out[r] = rank r's communicator.  pif_allreduce_f64: in-place
+ * sum of `count` doubles on `stream` (device memory of the comm's device);
+ * every rank must call it, each from its own thread.  libnccl.so.2 is opened at
+ * run time (the instance torch loaded, if any); pif_nccl_version reports it. */
+typedef struct pif_comm_s *pif_comm_t;
+int pif_nccl_version(int *version);
+int pif_comm_init_all(int ndev, const int *devices, pif_comm_t *comms_out);
+int pif_allreduce_f64(pif_comm_t comm, double *buf, int64_t count, void *stream);
+int pif_comm_destroy(pif_comm_t comm);
+
 /* cuFFT stage timing (the north star's "cuFFT call timed separately";
  * the reference times its fftn/ifftn inside Scatter/Gather, strategies.py:158-170).
  * pif_fft_timing(plan, slots): record CUDA events around each of the next

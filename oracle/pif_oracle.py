@@ -523,10 +523,11 @@ class PDRun:
         E_at = self._timed("interp", lambda: self._par(
             lambda r: interp3(plan, grids, prep_points(self.xs[r], self.L))))
 
-        def push():
-            for r in range(self.ranks):
-                self.xs[r], self.vs[r] = boris_push(self.xs[r], self.vs[r], E_at[r], self.q,
-                                                    self.m, self.B, self.e_kind, self.dt, self.L)
-        self._timed("push", push)
+        def push(r):
+            # each rank thread pushes its own slice, as the reference's rank
+            # threads do (numpy releases the GIL inside the array kernels)
+            self.xs[r], self.vs[r] = boris_push(self.xs[r], self.vs[r], E_at[r], self.q,
+                                                self.m, self.B, self.e_kind, self.dt, self.L)
+        self._timed("push", lambda: self._par(push))
         self.rho = self._solve()
         return field_energy(poisson_efield(self.rho, self.L), self.L)

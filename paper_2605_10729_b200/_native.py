@@ -81,6 +81,12 @@ SIGNATURES = {
     "pif_type1_complex_sorted": ([_P, _SOA, _P, _P, _P, _P], _I),
     "pif_type2_complex_sorted": ([_P, _P, _SOA, _P, _P], _I),
     "pif_sample_landau_axis": ([_P, _P, _I64, _I64, _D, _D, _D, _P, _I64, _P, _P], _I),
+    "pif_set_deterministic": ([_P, _I], _I),
+    "pif_is_deterministic": ([_P], _I),
+    "pif_nccl_version": ([ctypes.POINTER(ctypes.c_int)], _I),
+    "pif_comm_init_all": ([_I, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_P)], _I),
+    "pif_allreduce_f64": ([_P, _P, _I64, _P], _I),
+    "pif_comm_destroy": ([_P], _I),
     "pif_fft_timing": ([_P, _I], _I),
     "pif_fft_times": ([_P, _D3, _D3, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)],
                       _I),

@@ -6,8 +6,14 @@ path only needs ``allreduce_sum`` (strategies.py:124-128, 162-164), so this
 module keeps the same facade — ``Comm`` (rank, size, label, allreduce_sum),
 ``CallLog``, ``RankContext``, ``spawn_spmd``, the error types — over:
 
-* ``ThreadTransport``: ranks are threads of this process (spawn_spmd), each
-  driving its own GPU; the allreduce is a fixed-order binary tree
+* ``NcclThreadTransport``: ranks are threads of this process (spawn_spmd),
+  each driving its own GPU; the allreduce is one in-place ``ncclAllReduce``
+  per call on the rank's stream, over communicators made by one
+  ``ncclCommInitAll`` (libpifb200 ``pif_comm_init_all`` / ``pif_allreduce_f64``),
+  so CUDA graphs can capture it.  The default whenever every rank has a GPU of
+  its own.
+* ``ThreadTransport``: the same thread ranks when GPUs are shared (or none):
+  a rendezvous whose last arrival reduces in fixed binary-tree order
   (comm.py:329-339 semantics) over numpy arrays or CUDA tensors.
 * ``TorchDistTransport``: one process per GPU (torchrun), the allreduce is one
   in-place NCCL ``all_reduce`` over NVLink/NVSwitch (gloo for CPU tests).
@@ -172,6 +178,54 @@ def _reduce_any(ordered):
     return tree_sum([np.asarray(a) for a in ordered])
 
 
+class NcclThreadTransport:
+    """Thread ranks with one GPU each; allreduce = ncclAllReduce (in place, on
+    the calling thread's current stream).  numpy values go through a device
+    copy of the rank's GPU."""
+
+    def __init__(self, job: _Job, size: int, devices: list, label: str = "world"):
+        import ctypes
+
+        from . import _native
+        self.job, self.size, self.label = job, size, label
+        self.devices = [int(d) for d in devices]
+        lib = _native.load()
+        arr = (ctypes.c_int * size)(*self.devices)
+        out = (ctypes.c_void_p * size)()
+        _native.check(lib.pif_comm_init_all(size, arr, out), "pif_comm_init_all")
+        self._comms = list(out)
+        self._lib = lib
+
+    def allreduce(self, rank: int, value):
+        import torch
+
+        from . import _native
+        dev = torch.device("cuda", self.devices[rank])
+        if type(value).__module__.startswith("torch"):
+            t = value
+            if t.device != dev or t.dtype != torch.float64 or not t.is_contiguous():
+                raise CommError(f"rank {rank}: NCCL allreduce needs a contiguous float64 "
+                                f"tensor on {dev}, got {t.dtype} on {t.device}")
+            _native.check(self._lib.pif_allreduce_f64(self._comms[rank], t.data_ptr(), t.numel(),
+                                                      _native.stream_handle(dev)),
+                          "pif_allreduce_f64")
+            return t
+        arr = np.asarray(value)
+        cplx = np.iscomplexobj(arr)
+        flat = np.ascontiguousarray(arr, dtype=np.complex128 if cplx else np.float64)
+        t = torch.from_numpy(flat.view(np.float64).reshape(-1).copy()).to(dev)
+        _native.check(self._lib.pif_allreduce_f64(self._comms[rank], t.data_ptr(), t.numel(),
+                                                  _native.stream_handle(dev)), "pif_allreduce_f64")
+        out = t.cpu().numpy()
+        return (out.view(np.complex128) if cplx else out).reshape(arr.shape)
+
+    def close(self):
+        for c in self._comms:
+            if c:
+                self._lib.pif_comm_destroy(c)
+        self._comms = [None] * self.size
+
+
 # ---------------------------------------------------------------------------
 # torch.distributed transport (NCCL on GPUs, gloo on CPU)
 # ---------------------------------------------------------------------------
@@ -217,10 +271,13 @@ class Comm:
     def transport(self):
         return self._t
 
-    def allreduce_sum(self, values):
+    def allreduce_sum(self, values, log: bool = True):
         """Element-wise sum over ranks.  numpy in -> new numpy out (reference
-        semantics); torch tensor in -> reduced in place and returned."""
-        self._t.job.log(self.rank, "allreduce", self.label, -1, _nbytes(values))
+        semantics); torch tensor in -> reduced in place and returned.
+        log=False: not recorded in the CallLog (a CUDA-graph capture, whose
+        replays are logged instead)."""
+        if log:
+            self._t.job.log(self.rank, "allreduce", self.label, -1, _nbytes(values))
         if self.size == 1:
             if type(values).__module__.startswith("torch"):
                 return values
@@ -279,15 +336,41 @@ def _rank_device(rank: int):
     return None
 
 
+def _default_backend(num_ranks: int) -> str:
+    """"nccl" when every rank thread gets a GPU of its own, else "threads"
+    (env PIF_SPMD_BACKEND overrides)."""
+    want = os.environ.get("PIF_SPMD_BACKEND", "").strip().lower()
+    if want in ("nccl", "threads"):
+        return want
+    try:
+        import torch
+        if num_ranks > 1 and torch.cuda.is_available() and \
+                num_ranks <= torch.cuda.device_count():
+            return "nccl"
+    except Exception:  # noqa: BLE001
+        pass
+    return "threads"
+
+
 def spawn_spmd(num_ranks: int, program: Callable[[RankContext], Any], *,
-               watchdog: float = 60.0, call_log: CallLog | None = None) -> list:
+               watchdog: float = 60.0, call_log: CallLog | None = None,
+               backend: str | None = None) -> list:
     """Run `program` on `num_ranks` in-process rank threads (comm.py:483-528
     contract: results in rank order, any failure aborts the job and names the
-    rank).  Rank r drives CUDA device r mod device_count."""
+    rank).  Rank r drives CUDA device r mod device_count.  backend "nccl"
+    (default when each rank has its own GPU) reduces with ncclAllReduce over
+    communicators from one ncclCommInitAll; "threads" with the fixed-order
+    tree rendezvous."""
     if num_ranks < 1:
         raise ValueError(f"num_ranks must be >= 1, got {num_ranks}")
+    backend = backend or _default_backend(num_ranks)
+    if backend not in ("nccl", "threads"):
+        raise ValueError(f"unknown spmd backend {backend!r}")
     job = _Job(watchdog, call_log)
-    transport = ThreadTransport(job, num_ranks, "world")
+    if backend == "nccl" and num_ranks > 1:
+        transport = NcclThreadTransport(job, num_ranks, list(range(num_ranks)), "world")
+    else:
+        transport = ThreadTransport(job, num_ranks, "world")
     results: list = [None] * num_ranks
 
     def worker(rank):
@@ -306,8 +389,19 @@ def spawn_spmd(num_ranks: int, program: Callable[[RankContext], Any], *,
                for r in range(num_ranks)]
     for t in threads:
         t.start()
-    for t in threads:
-        t.join()
+    # a rank that died leaves its peers waiting inside a collective (NCCL
+    # kernels never time out): give them `watchdog` seconds, then report
+    failed_at = None
+    while any(t.is_alive() for t in threads):
+        for t in threads:
+            t.join(timeout=0.05)
+        if job.failed.is_set():
+            failed_at = failed_at or time.monotonic()
+            if time.monotonic() - failed_at > watchdog:
+                break
+    hung = [t for t in threads if t.is_alive()]
+    if not hung and isinstance(transport, NcclThreadTransport):
+        transport.close()
     if job.failures:
         dead = [(r, e) for r, e in job.failures if isinstance(e, DeadlockError)]
         other = [(r, e) for r, e in job.failures if not isinstance(e, DeadlockError)]

@@ -54,7 +54,8 @@ int dalloc(Plan &p, T **ptr, size_t count) {
 void release(Plan &p) {
     void *ptrs[] = {p.deconv, p.kvec, p.grid, p.spec, p.field, p.field3, p.emodes, p.cgrid,
                     p.cell_count, p.cell_start, p.scan_tmp, p.work, p.partials, p.maxbits,
-                    p.shape_tab, p.items, p.seg_parts, p.seg_off, p.ring_scratch, p.wcache};
+                    p.shape_tab, p.items, p.seg_parts, p.seg_off, p.ring_scratch, p.wcache,
+                    p.dbuf, p.det_keys, p.det_iota, p.det_tmp};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     if (p.d2z) cufftDestroy(p.d2z);
@@ -394,6 +395,19 @@ int pif_interp_push_perm(pif_plan_t plan, const pif_soa_t *src, const int32_t *p
     return rc;
 }
 
+
+int pif_set_deterministic(pif_plan_t plan, int enable) {
+    if (!plan) return pif::bad("null plan");
+    Plan &p = plan->p;
+    if (enable && !pif::det_supported(p))
+        return pif::bad("deterministic mode covers the DMMA kernels only: window width w <= 8 "
+                        "(eps >= 1e-7)");
+    p.det = enable != 0;
+    if (p.det) p.wcache_valid = false;
+    return PIF_OK;
+}
+
+int pif_is_deterministic(pif_plan_t plan) { return plan && plan->p.det ? 1 : 0; }
 
 int pif_fft_timing(pif_plan_t plan, int slots) {
     if (!plan) return pif::bad("null plan");

@@ -292,21 +292,38 @@ __device__ __forceinline__ void chunk_weights_async(WarpChunk &st, const double 
 // (slot k&7), which is flushed with REDG.ADD.F64 and reused for plane k+8.
 // ----------------------------------------------------------------------------
 
-template <int W>
+// Deterministic mode (pif_set_deterministic): instead of REDG into the grid,
+// plane k of the item goes to its own slice of the plane buffer,
+// dbuf[((item * 64 + a * 8 + b) * dstride) + (k - k0)], and det_reduce_kernel
+// sums the slices of every grid point in a fixed order.
+struct DetOut {
+    double *buf = nullptr;   // null: atomics into the grid
+    int64_t stride = 0;      // planes per (item, a, b) row: seg + 7
+};
+
+template <int W, bool DET>
 __device__ __forceinline__ void spread_flush_plane(double (&acc)[8][2], int k, int c4, int ix,
-                                                   int64_t yrow, int n, double *grid) {
+                                                   int64_t yrow, int n, double *grid,
+                                                   const DetOut &det, int64_t drow, int k0) {
     const int s = k & 7;
     if (c4 == (s >> 1)) {
         const int j = s & 1;
-        const int z = k;   // cells of an item never wrap: k < n
-        const int64_t nn = (int64_t)n * n;
-        int64_t off = ((int64_t)ix * n + yrow) * n + z;
+        if (DET) {
+            // drow = (item * 64 + r) * stride: this lane's b = r rows, a-major
 #pragma unroll
-        for (int a = 0; a < W; ++a) {
-            const double v = j ? acc[a][1] : acc[a][0];
-            PIF_CHECK(off == ((int64_t)((ix + a) % n) * n + yrow) * n + z);
-            if (v != 0.0) atomicAdd(grid + off, v);
-            off += (ix + a + 1 == n) ? nn - (int64_t)n * nn : nn;   // x wraps once (w <= n)
+            for (int a = 0; a < W; ++a)
+                det.buf[drow + (int64_t)a * 8 * det.stride + (k - k0)] = j ? acc[a][1] : acc[a][0];
+        } else {
+            const int z = k;   // cells of an item never wrap: k < n
+            const int64_t nn = (int64_t)n * n;
+            int64_t off = ((int64_t)ix * n + yrow) * n + z;
+#pragma unroll
+            for (int a = 0; a < W; ++a) {
+                const double v = j ? acc[a][1] : acc[a][0];
+                PIF_CHECK(off == ((int64_t)((ix + a) % n) * n + yrow) * n + z);
+                if (v != 0.0) atomicAdd(grid + off, v);
+                off += (ix + a + 1 == n) ? nn - (int64_t)n * nn : nn;   // x wraps once (w <= n)
+            }
         }
 #pragma unroll
         for (int a = 0; a < 8; ++a) {
@@ -324,7 +341,7 @@ constexpr int kSpreadUnroll = PIF_SPREAD_UNROLL;
 #define PIF_SPREAD_MINB 4
 #endif
 
-template <int W>
+template <int W, bool DET>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, PIF_SPREAD_MINB)
 spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
                   const double *__restrict__ pz, const int64_t *__restrict__ pid,
@@ -332,7 +349,7 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
                   const int32_t *__restrict__ cell_start, double *__restrict__ grid, int n,
                   int seg, int nseg, double h, double beta, const EsPoly poly, unsigned int *work,
                   const int2 *__restrict__ items, const int *__restrict__ n_items,
-                  double *__restrict__ wc, int64_t wstride) {
+                  double *__restrict__ wc, int64_t wstride, const DetOut det) {
     const int nitems = *n_items;
     const double rh = __drcp_rn(h);
     __shared__ WarpChunk stage[kWarpsPerBlock];
@@ -357,6 +374,7 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
         const int pbeg = cell_start[base + k0] + it.y * kItemParticles;
         const int pend = min(pbeg + kItemParticles, cell_start[base + k1]);
         const int64_t yrow = (iy + r) % n;   // this lane's footprint row b = r
+        const int64_t drow = DET ? ((int64_t)item * 64 + r) * det.stride : 0;
 
         double acc[8][2];
 #pragma unroll
@@ -390,7 +408,7 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
             int j = 0;
             while (j < cnt) {
                 if (pos + j >= cell_end) {
-                    spread_flush_plane<W>(acc, k, c4, ix, yrow, n, grid);
+                    spread_flush_plane<W, DET>(acc, k, c4, ix, yrow, n, grid, det, drow, k0);
                     ++k;
                     cell_end = next_end;
                     next_end = cell_start[base + min(k + 2, k1)];
@@ -423,18 +441,58 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
             }
             __syncwarp();
         }
-        for (; k < k1; ++k) spread_flush_plane<W>(acc, k, c4, ix, yrow, n, grid);
+        for (; k < k1; ++k) spread_flush_plane<W, DET>(acc, k, c4, ix, yrow, n, grid, det, drow, k0);
         // pending planes k1 .. k1+6
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
             const int s = 2 * c4 + j;
-            const int z = (k1 + ((s - k1) & 7)) % n;
+            const int dz = (s - k1) & 7;   // dz == 7: plane k1 + 7, flushed with cell k1 - 1
+            const int z = (k1 + dz) % n;
 #pragma unroll
             for (int a = 0; a < W; ++a) {
                 const double v = acc[a][j];
-                if (v != 0.0) atomicAdd(grid + ((int64_t)((ix + a) % n) * n + yrow) * n + z, v);
+                if (DET) {
+                    if (dz < 7)
+                        det.buf[drow + (int64_t)a * 8 * det.stride + (k1 + dz - k0)] = v;
+                } else if (v != 0.0) {
+                    atomicAdd(grid + ((int64_t)((ix + a) % n) * n + yrow) * n + z, v);
+                }
             }
         }
+    }
+}
+
+// Deterministic plane reduction: grid point (X, Y, Z) = sum over the footprint
+// rows (a, b) of column (X - a, Y - b), over the (at most two) z-segments of
+// that column whose footprint [k0, k1 + 7) covers Z (the one holding Z and the
+// previous one, cyclically; seg >= 8), over each segment's parts in order.
+// Fixed order, so the grid is the same bits on every run.
+__global__ void det_reduce_kernel(const double *__restrict__ dbuf, int64_t stride,
+                                  const int *__restrict__ seg_off, const int *__restrict__ seg_parts,
+                                  int n, int seg, int nseg, int w, double *__restrict__ grid) {
+    const int64_t n3 = (int64_t)n * n * n;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n3;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int Z = (int)(idx % n), Y = (int)((idx / n) % n), X = (int)(idx / ((int64_t)n * n));
+        const int s0 = Z / seg, sp = (s0 + nseg - 1) % nseg;
+        double acc = 0.0;
+        for (int a = 0; a < w; ++a) {
+            const int ix = (X - a + n) % n;
+            for (int b = 0; b < w; ++b) {
+                const int col = ix * n + (Y - b + n) % n;
+                for (int t = 0; t < 2; ++t) {
+                    const int sg = t ? sp : s0;
+                    if (t && sp == s0) break;
+                    const int k0 = sg * seg, len = min(k0 + seg, n) - k0;
+                    const int sidx = col * nseg + sg;
+                    const int first = seg_off[sidx], cnt = seg_parts[sidx];
+                    for (int pz = (Z - k0 + n) % n; pz < len + 7; pz += n)
+                        for (int j = 0; j < cnt; ++j)
+                            acc += dbuf[((int64_t)(first + j) * 64 + a * 8 + b) * stride + pz];
+                }
+            }
+        }
+        grid[idx] = acc;
     }
 }
 
@@ -1493,6 +1551,8 @@ PushParams make_push(const Plan &p, double half, double dt, const double *tq, co
 // launchers
 // ============================================================================
 
+bool det_supported(const Plan &p) { return fast_path_ok(p); }
+
 int launch_wrap(Plan &p, double *x, double *y, double *z, int64_t M, cudaStream_t s) {
     p.wcache_valid = false;
     if (M == 0) return PIF_OK;
@@ -1601,6 +1661,43 @@ int launch_load_aos(Plan &p, const double *x, const double *v, int64_t id0, pif_
     return fail_cuda(cudaGetLastError(), "load_aos_kernel");
 }
 
+__global__ void iota_kernel(int32_t *out, int64_t M) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (int32_t)i;
+}
+
+// perm = stable argsort of the cell keys (CUB LSD radix sort is stable)
+int det_sort_perm(Plan &p, const int32_t *key, int64_t M, int32_t *perm, cudaStream_t s) {
+    int bits = 1;
+    while ((int64_t(1) << bits) < p.n3) ++bits;
+    size_t tmp = 0;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, tmp, key, p.det_keys, p.det_iota, perm,
+                                                    (int)M, 0, bits, s);
+    if (e != cudaSuccess) return fail_cuda(e, "radix sort size");
+    if (M > p.det_cap || tmp > p.det_tmp_bytes) {
+        cudaFree(p.det_keys);
+        cudaFree(p.det_iota);
+        cudaFree(p.det_tmp);
+        p.det_keys = nullptr;
+        p.det_iota = nullptr;
+        p.det_tmp = nullptr;
+        p.det_cap = 0;
+        p.det_tmp_bytes = 0;
+        e = cudaMalloc(&p.det_keys, sizeof(int32_t) * M);
+        if (e == cudaSuccess) e = cudaMalloc(&p.det_iota, sizeof(int32_t) * M);
+        if (e == cudaSuccess) e = cudaMalloc(&p.det_tmp, tmp);
+        if (e != cudaSuccess) return fail_cuda(e, "deterministic binning scratch");
+        p.det_cap = M;
+        p.det_tmp_bytes = tmp;
+    }
+    iota_kernel<<<grid_for(M, 256, p.sm_count), 256, 0, s>>>(p.det_iota, M);
+    tmp = p.det_tmp_bytes;
+    e = cub::DeviceRadixSort::SortPairs(p.det_tmp, tmp, key, p.det_keys, p.det_iota, perm, (int)M,
+                                        0, bits, s);
+    return fail_cuda(e, "radix sort");
+}
+
 int launch_bin_perm(Plan &p, const int32_t *key, const int32_t *rank, int64_t M, int32_t *perm,
                     cudaStream_t s) {
     p.wcache_valid = false;
@@ -1608,7 +1705,12 @@ int launch_bin_perm(Plan &p, const int32_t *key, const int32_t *rank, int64_t M,
     cudaError_t e = cub::DeviceScan::ExclusiveSum(p.scan_tmp, tmp, p.cell_count, p.cell_start,
                                                   (int)(p.n3 + 1), s);
     if (e != cudaSuccess) return fail_cuda(e, "cell scan");
-    if (M > 0) {
+    if (M > 0 && p.det) {
+        // stable binning: perm = indices sorted by key, ties in index order
+        // (the atomic ranks would order a cell's particles by arrival)
+        const int rc = det_sort_perm(p, key, M, perm, s);
+        if (rc != PIF_OK) return rc;
+    } else if (M > 0) {
         bin_perm_kernel<<<grid_for(M, 256, p.sm_count), 256, 0, s>>>(key, rank, p.cell_start, M,
                                                                       perm);
         e = cudaGetLastError();
@@ -1634,35 +1736,44 @@ int launch_spread(Plan &p, const pif_soa_t &P, const int32_t *perm, const double
         if (e != cudaSuccess) return fail_cuda(e, "zero work counter");
         const int threads = kWarpsPerBlock * 32;
         // keep this spread's window weights for the gather at the same positions
-        double *wc = (p.wcache_on && ensure_wcache(p, P.count) == PIF_OK) ? p.wcache : nullptr;
+        double *wc = (!p.det && p.wcache_on && ensure_wcache(p, P.count) == PIF_OK) ? p.wcache
+                                                                                : nullptr;
         if (wc) {
             p.wcache_valid = true;
             p.wcache_x = P.x;
             p.wcache_perm = perm;
             p.wcache_count = P.count;
         }
+        DetOut det;
+        if (p.det) {
+            // one slice of (seg + 7) planes x 64 rows per work item, zeroed (an
+            // item flushes only the planes from its first non-empty cell on)
+            det.stride = p.seg + 7;
+            const int64_t need = p.items_cap * 64 * det.stride;
+            if (need > p.dbuf_cap) {
+                if (p.dbuf) cudaFree(p.dbuf);
+                p.dbuf = nullptr;
+                p.dbuf_cap = 0;
+                e = cudaMalloc(&p.dbuf, sizeof(double) * need);
+                if (e != cudaSuccess) return fail_cuda(e, "deterministic plane buffer");
+                p.dbuf_cap = need;
+            }
+            e = cudaMemsetAsync(p.dbuf, 0, sizeof(double) * need, s);
+            if (e != cudaSuccess) return fail_cuda(e, "zero plane buffer");
+            det.buf = p.dbuf;
+            wc = nullptr;
+            p.wcache_valid = false;
+        }
 #define PIF_SPREAD_CASE(W)                                                                   \
     case W: {                                                                                \
-        auto k = spread_mma_kernel<W>;                                                      \
+        auto k = p.det ? spread_mma_kernel<W, true> : spread_mma_kernel<W, false>;          \
         int blocks = persistent_blocks(k, threads, 0, p.sm_count);                           \
         k<<<blocks, threads, 0, s>>>(P.x, P.y, P.z, P.id, perm, strengths, q, p.cell_start,   \
                                      p.grid,                                                 \
                                      p.n, p.seg, nseg, p.h, p.beta, poly, p.work, p.items,   \
-                                     nitems, wc, P.count);                                   \
+                                     nitems, wc, P.count, det);                              \
         break;                                                                               \
     }
-        switch (p.w) {
-            PIF_SPREAD_CASE(2)
-            PIF_SPREAD_CASE(3)
-            PIF_SPREAD_CASE(4)
-            PIF_SPREAD_CASE(5)
-            PIF_SPREAD_CASE(6)
-            PIF_SPREAD_CASE(7)
-            PIF_SPREAD_CASE(8)
-            default:
-                set_error("unsupported window width");
-                return PIF_ERR_VALUE;
-        }
 #undef PIF_SPREAD_CASE
     } else if (ring_path_ok(p) && p.density >= kRingSpreadMinDensity) {
         const int nseg = (p.n + p.seg - 1) / p.seg;

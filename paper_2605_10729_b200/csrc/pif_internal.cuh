@@ -91,6 +91,15 @@ struct Plan {
     int64_t bytes = 0;
     // optional cuFFT timing (bench.py): event pairs around each D2Z / Z2D exec,
     // slot k of each ring holds the k-th exec since the last pif_fft_times
+    // deterministic mode (pif_set_deterministic): stable binning + fixed-order
+    // plane reduction instead of REDG, diagnostics from a fixed-order pass
+    bool det = false;
+    double *dbuf = nullptr;        // per-item plane slices of the spread
+    int64_t dbuf_cap = 0;
+    int32_t *det_keys = nullptr, *det_iota = nullptr;
+    void *det_tmp = nullptr;
+    size_t det_tmp_bytes = 0;
+    int64_t det_cap = 0;
     cudaEvent_t *fft_ev = nullptr;  // [d2z begin, d2z end] x slots, then z2d pairs
     int fft_slots = 0, fft_nd = 0, fft_nz = 0;
     EsPolyHost poly{};              // interior weight polynomials for w <= 8
@@ -110,6 +119,7 @@ int launch_bin_keys(Plan &p, const pif_soa_t &src, int32_t *key, int32_t *rank, 
 int launch_bin_scatter(Plan &p, const pif_soa_t &src, pif_soa_t &dst, const int32_t *key,
                        const int32_t *rank, bool vel, cudaStream_t s);
 int build_items(Plan &p, int64_t M, cudaStream_t s);
+bool det_supported(const Plan &p);   // the DMMA (w <= 8) kernels serve this plan
 int debug_phase_cycles(unsigned long long *out);
 int launch_soa_to_aos(Plan &p, const pif_soa_t &P, int64_t id0, double *ox, double *ov,
                       cudaStream_t s);

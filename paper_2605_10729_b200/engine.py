@@ -38,7 +38,7 @@ class PifEngine:
     the fine grid, spectra, field grid and cell tables."""
 
     def __init__(self, plan, count: int, device, *, q: float, m: float, externals, dt: float,
-                 shape: str = "delta", comm=None):
+                 shape: str = "delta", comm=None, deterministic: bool | None = None):
         torch = require_cuda()
         if shape not in _native.SHAPE:
             raise ValueError(f"unknown shape {shape!r}")
@@ -69,6 +69,22 @@ class PifEngine:
         self.dtimers = DeviceTimers(enabled=False)
         self.launches = 0   # native kernel launches issued (for bench accounting)
         self.weight_cache = self._enable_weight_cache()
+        self.deterministic = False
+        if deterministic is None:
+            import os
+            deterministic = os.environ.get("PIF_DETERMINISTIC", "0").strip() not in (
+                "0", "", "false", "off")
+        self.set_deterministic(deterministic)
+
+    def set_deterministic(self, on: bool):
+        """Bit-reproducible stepping (pif_set_deterministic): stable binning,
+        fixed-order plane reduction in the spread, diagnostics from a
+        fixed-order pass.  Raises ValueError for windows wider than 8 (the
+        DMMA kernels are the only deterministic ones)."""
+        _native.call("pif_set_deterministic", self.handle, 1 if on else 0)
+        self.deterministic = bool(on)
+        if on:
+            self.weight_cache = False
 
     def configure(self, *, q: float, m: float, externals, dt: float, shape: str = "delta"):
         """(Re)set the per-run constants: charge/mass per particle, the Boris
@@ -139,11 +155,13 @@ class PifEngine:
         return _native.soa_from_store(p.buf[i], p.ids[i], p.count)
 
     @classmethod
-    def for_ensemble(cls, ens, plan, externals, dt, shape="delta", comm=None, device=None):
+    def for_ensemble(cls, ens, plan, externals, dt, shape="delta", comm=None, device=None,
+                     deterministic=None):
         from ._device import default_device
         dev = device if device is not None else default_device(ens.x)
         eng = cls(plan, ens.count, dev, q=ens.q_per_particle, m=ens.m_per_particle,
-                  externals=externals, dt=dt, shape=shape, comm=comm)
+                  externals=externals, dt=dt, shape=shape, comm=comm,
+                  deterministic=deterministic)
         eng.load(ens.x, ens.v, np.arange(ens.count, dtype=np.int64))
         return eng
 
@@ -250,7 +268,7 @@ class PifEngine:
 
     def allreduce(self):
         if self.comm is not None:
-            self.comm.allreduce_sum(self.red)
+            self.comm.allreduce_sum(self.red, log=not getattr(self, "_capturing", False))
 
     def solve_fields(self):
         """finish_deposit + Poisson + energy + guard + padded spectra + Z2D."""
@@ -268,6 +286,8 @@ class PifEngine:
                      self.parts.rank.data_ptr(), self.diag.data_ptr(), self._stream())
         self.parts.swap()
         self.launches += 2
+        if self.deterministic:      # the fused sums depend on the work-item schedule
+            self.particle_diag()
 
     def rebin(self):
         """Scan the cell counts emitted by interp_push and rebuild perm."""
@@ -302,6 +322,7 @@ class PifEngine:
             graph = timers is None and steps >= 8 and self._graph_ok()
         self.particle_diag()
         self._solve(dt, record_slot=0)
+        self.graph_pairs = 0        # two-step graph replays of the last run
         i = 0
         if graph:
             # two eager steps warm every allocation / plan, then capture
@@ -315,6 +336,7 @@ class PifEngine:
                 g = self._capture_pair(i + 1)
                 for _ in range(pairs):
                     g.replay()
+                    self.graph_pairs += 1
                     if self.comm is not None:   # the graph's two collectives
                         self.comm.log_replayed_allreduce(self.red, 2)
                 i += 2 * pairs
@@ -327,9 +349,11 @@ class PifEngine:
         return self.rec
 
     def _graph_ok(self) -> bool:
-        # NCCL collectives can be captured, the in-process thread transport cannot
-        from .comm import TorchDistTransport
-        return self.comm is None or isinstance(self.comm.transport, TorchDistTransport)
+        # NCCL collectives (torchrun ranks or NCCL thread ranks) can be
+        # captured; the host-side tree rendezvous of shared-GPU thread ranks cannot
+        from .comm import NcclThreadTransport, TorchDistTransport
+        return self.comm is None or self.comm.size == 1 or isinstance(
+            self.comm.transport, (TorchDistTransport, NcclThreadTransport))
 
     def _capture_pair(self, first_slot: int):
         """CUDA graph of two full steps recording into rec[slot], rec[slot+1]
@@ -341,13 +365,14 @@ class PifEngine:
         side.wait_stream(torch.cuda.current_stream(self.device))
         g = torch.cuda.CUDAGraph()
         # capture records the collectives without running them: the call log
-        # gets its entries per replay instead (run())
-        log = self.comm.transport.job.call_log if self.comm is not None else None
-        if self.comm is not None:
-            self.comm.transport.job.call_log = None
+        # gets its entries per replay instead (run()); the job's log is shared
+        # by all rank threads, so this rank just stops logging while it captures
+        self._capturing = True
         try:
             with torch.cuda.stream(side):
-                with torch.cuda.graph(g, stream=side):
+                # thread_local: other rank threads keep allocating / launching
+                # eagerly while this one captures
+                with torch.cuda.graph(g, stream=side, capture_error_mode="thread_local"):
                     for _ in range(2):
                         self.gather_push()
                         self.deposit()
@@ -359,8 +384,7 @@ class PifEngine:
                         self.rec.index_copy_(0, self._slot, self._row)
                         self._slot += 1
         finally:
-            if self.comm is not None:
-                self.comm.transport.job.call_log = log
+            self._capturing = False
         torch.cuda.current_stream(self.device).wait_stream(side)
         return g
 

@@ -39,6 +39,11 @@ class RunSetup:
     # libm ulps); "auto": device above 2^22 particles, where the reference's
     # per-rank materialisation of the global ensemble stops fitting host memory
     sampler: str = "auto"
+    # bit-reproducible stepping (stable binning + fixed-order plane reduction,
+    # PifEngine.set_deterministic): the reference's runs are bit-identical by
+    # construction (test_strategies.py:57-62, 405-409); off by default, the
+    # atomic spread is the fast path
+    deterministic: bool = False
 
 
 @dataclass(frozen=True)
@@ -103,7 +108,8 @@ def _run_replicated(setup: RunSetup, comm: Comm | None, timers: Timers | None,
         "cuda", torch.cuda.current_device())
     with torch.cuda.device(dev):
         eng = PifEngine(plan, hi - lo, dev, q=q, m=m, externals=externals, dt=spec.dt,
-                        shape=setup.shape, comm=comm)
+                        shape=setup.shape, comm=comm,
+                        deterministic=True if setup.deterministic else None)
         if on_device:
             eng.load_sampled(spec, (lo, hi))
         else:

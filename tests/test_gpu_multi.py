@@ -88,3 +88,57 @@ def test_cli_under_torchrun_two_gpus(cuda, tmp_path):
     assert np.max(np.abs(got - ref) / np.abs(ref)) <= 1e-10
     with open(out / "timers.csv") as f:
         assert {r["rank"] for r in csv.DictReader(f)} == {"0", "1"}
+
+
+# ---------------------------------------------------------------------------
+# the reference's in-process model: spawn_spmd thread ranks over NCCL
+# (comm.py:483-528; communicators from one ncclCommInitAll, pif_comm_init_all)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_spawn_spmd_thread_ranks_run_pd_over_nccl_with_graphs(P, cuda):
+    torch = cuda
+    if torch.cuda.device_count() < P:
+        pytest.skip(f"needs {P} GPUs")
+    import paper_2605_10729_b200 as pb
+    from paper_2605_10729_b200 import comm
+    spec = pb.landau_spec(N=16, ppm=16, dt=0.05, steps=20, seed=0)
+    setup = pb.RunSetup(spec=spec, eps=1e-7)
+    log = comm.CallLog()
+    seen = []
+
+    def program(ctx):
+        seen.append(type(ctx.world.transport).__name__)
+        return pb.run_particle_decomposition(setup, ctx)
+
+    res = pb.spawn_spmd(P, program, call_log=log)
+    assert set(seen) == {"NcclThreadTransport"}
+    for rank, r in enumerate(res):
+        assert r["engine"].graph_pairs > 0              # steps replayed from CUDA graphs
+        assert r["engine"].device.index == rank
+    cfg = golden("config1.npz")
+    got = np.array([[r.field_energy, r.kinetic_energy, r.total_energy]
+                    for r in [res[0]["initial"]] + res[0]["records"]])
+    ref = cfg["landau_pd2_trace" if P == 2 else "landau_trace"][:, 2:5]
+    assert np.max(np.abs(got - ref) / np.abs(ref)) <= 1e-10
+    assert log.primitives() == {"allreduce"}
+    assert len(log.records) == P * (spec.steps + 1)     # one collective per step and rank
+
+
+def test_nccl_thread_transport_reduces_numpy_and_tensors(cuda):
+    torch = cuda
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    import paper_2605_10729_b200 as pb
+
+    def program(ctx):
+        r = ctx.world_rank
+        a = ctx.world.allreduce_sum(np.array([1.0 + r, 2.0 * r, 1j * r]))
+        t = torch.full((5,), float(r + 1), dtype=torch.float64, device=ctx.device)
+        ctx.world.allreduce_sum(t)
+        return a, t.cpu().numpy()
+
+    out = pb.spawn_spmd(2, program, backend="nccl")
+    for a, t in out:
+        assert np.array_equal(a, np.array([3.0, 2.0, 1j]))
+        assert np.array_equal(t, np.full(5, 3.0))
