@@ -1774,7 +1774,25 @@ int launch_spread(Plan &p, const pif_soa_t &P, const int32_t *perm, const double
                                      nitems, wc, P.count, det);                              \
         break;                                                                               \
     }
+        switch (p.w) {
+            PIF_SPREAD_CASE(2)
+            PIF_SPREAD_CASE(3)
+            PIF_SPREAD_CASE(4)
+            PIF_SPREAD_CASE(5)
+            PIF_SPREAD_CASE(6)
+            PIF_SPREAD_CASE(7)
+            PIF_SPREAD_CASE(8)
+            default:
+                set_error("unsupported window width");
+                return PIF_ERR_VALUE;
+        }
 #undef PIF_SPREAD_CASE
+        if (p.det) {
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return fail_cuda(e, "spread kernel");
+            det_reduce_kernel<<<grid_for(p.n3, 256, p.sm_count), 256, 0, s>>>(
+                p.dbuf, det.stride, p.seg_off, p.seg_parts, p.n, p.seg, nseg, p.w, p.grid);
+        }
     } else if (ring_path_ok(p) && p.density >= kRingSpreadMinDensity) {
         const int nseg = (p.n + p.seg - 1) / p.seg;
         const int *nitems = p.seg_off + p.n_segs;
