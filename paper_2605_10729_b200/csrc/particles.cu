@@ -463,9 +463,9 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
 }
 
 // Deterministic plane reduction: grid point (X, Y, Z) = sum over the footprint
-// rows (a, b) of column (X - a, Y - b), over the (at most two) z-segments of
-// that column whose footprint [k0, k1 + 7) covers Z (the one holding Z and the
-// previous one, cyclically; seg >= 8), over each segment's parts in order.
+// rows (a, b) of column (X - a, Y - b), over the z-segments of that column
+// whose footprint [k0, k1 + 7) covers Z (cyclically), over each segment's
+// parts in order.
 // Fixed order, so the grid is the same bits on every run.
 __global__ void det_reduce_kernel(const double *__restrict__ dbuf, int64_t stride,
                                   const int *__restrict__ seg_off, const int *__restrict__ seg_parts,
@@ -474,15 +474,17 @@ __global__ void det_reduce_kernel(const double *__restrict__ dbuf, int64_t strid
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n3;
          idx += (int64_t)gridDim.x * blockDim.x) {
         const int Z = (int)(idx % n), Y = (int)((idx / n) % n), X = (int)(idx / ((int64_t)n * n));
-        const int s0 = Z / seg, sp = (s0 + nseg - 1) % nseg;
+        // the segment holding Z and the ones before it (cyclically) whose 7-plane
+        // tails may reach Z: a short last segment (n % seg < 7) lets the tail
+        // of the one before it wrap past it, so walk back up to 8 segments
+        const int s0 = Z / seg, nback = min(nseg, 8);
         double acc = 0.0;
         for (int a = 0; a < w; ++a) {
             const int ix = (X - a + n) % n;
             for (int b = 0; b < w; ++b) {
                 const int col = ix * n + (Y - b + n) % n;
-                for (int t = 0; t < 2; ++t) {
-                    const int sg = t ? sp : s0;
-                    if (t && sp == s0) break;
+                for (int t = 0; t < nback; ++t) {
+                    const int sg = (s0 - t + nseg) % nseg;
                     const int k0 = sg * seg, len = min(k0 + seg, n) - k0;
                     const int sidx = col * nseg + sg;
                     const int first = seg_off[sidx], cnt = seg_parts[sidx];
