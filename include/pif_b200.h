@@ -101,6 +101,9 @@ int pif_bin_scatter(pif_plan_t plan, const pif_soa_t *src, pif_soa_t *dst, const
  * the particles out in cell order (pif_interp_push_perm). */
 int pif_bin_perm(pif_plan_t plan, const int32_t *key, const int32_t *rank, int64_t M,
                  int32_t *perm, void *stream);
+/* rank may be NULL: each particle then takes the next free slot of its cell
+ * from a per-cell cursor (warp-aggregated atomics), so producers of keys (the
+ * push kernels) only count and never wait on a returning atomic. */
 
 /* ---- type-1 spreading: replaces _kernels.spread_r (_kernels.py:57-96) ------
  * Reads cell-sorted particles (dst of pif_bin_scatter).  strengths == NULL
@@ -152,7 +155,9 @@ int pif_interp_push(pif_plan_t plan, pif_soa_t *sorted, double half, double dt,
                     const double tq[3], const double sq[3], int has_b, int e_kind,
                     int32_t *key, int32_t *rank, double *diag, void *stream);
 /* Same, reading src through perm and writing the updated particles (and ids)
- * to dst in that order (dst must not alias src); key/rank refer to dst. */
+ * to dst in that order (dst must not alias src); key/rank refer to dst.  rank
+ * may be NULL (then only the cell counts are incremented; pif_bin_perm with a
+ * NULL rank assigns the slots). */
 int pif_interp_push_perm(pif_plan_t plan, const pif_soa_t *src, const int32_t *perm,
                          pif_soa_t *dst, double half, double dt, const double tq[3],
                          const double sq[3], int has_b, int e_kind, int32_t *key, int32_t *rank,

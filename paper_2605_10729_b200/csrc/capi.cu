@@ -363,7 +363,7 @@ int pif_spread_sorted(pif_plan_t plan, const pif_soa_t *sorted, const double *st
 int pif_bin_perm(pif_plan_t plan, const int32_t *key, const int32_t *rank, int64_t M,
                  int32_t *perm, void *stream) {
     PLAN_CHECK();
-    if (M < 0 || M >= (int64_t)INT32_MAX || (M > 0 && (!key || !rank || !perm)))
+    if (M < 0 || M >= (int64_t)INT32_MAX || (M > 0 && (!key || !perm)))
         return pif::bad("invalid binning arguments");
     return pif::launch_bin_perm(p, key, rank, M, perm, s);
 }
@@ -384,7 +384,7 @@ int pif_interp_push_perm(pif_plan_t plan, const pif_soa_t *src, const int32_t *p
     pif_soa_t d = *dst;
     d.count = src->count;
     if (!pif::soa_ok(&d, true)) return pif::bad("invalid destination view");
-    if (src->count > 0 && (!key || !rank || !perm)) return pif::bad("missing key/rank/perm");
+    if (src->count > 0 && (!key || !perm)) return pif::bad("missing key/perm");
     if (!diag) return pif::bad("null diag");
     if (e_kind != PIF_EXT_NONE && e_kind != PIF_EXT_QUADRUPOLE) return pif::bad("unknown e_kind");
     if (!(dt > 0)) return pif::bad("dt must be positive");

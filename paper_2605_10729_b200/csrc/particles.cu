@@ -139,6 +139,32 @@ __global__ void bin_perm_kernel(const int32_t *__restrict__ key, const int32_t *
     }
 }
 
+// rank-free variant: the in-cell slot comes from a cursor per cell (the count
+// table, zeroed after the scan); lanes of a warp holding the same key take
+// consecutive slots with one atomic (consecutive particles mostly share a
+// cell: they were written in cell order by the previous push)
+__global__ void bin_perm_cursor_kernel(const int32_t *__restrict__ key, int32_t *__restrict__ cursor,
+                                       const int32_t *__restrict__ start, int64_t M,
+                                       int32_t *__restrict__ perm) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x; j0 < M;
+         j0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = j0 + threadIdx.x;
+        const bool ok = j < M;
+        const int k = ok ? key[j] : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, k);
+        const int leader = __ffs(peers) - 1;
+        int base = 0;
+        if (ok && lane == leader) base = atomicAdd(&cursor[k], __popc(peers));
+        base = __shfl_sync(peers, base, leader);
+        if (ok) {
+            const int slot = start[k] + base + __popc(peers & ((1u << lane) - 1u));
+            PIF_CHECK(slot >= 0 && slot < M);
+            perm[slot] = (int32_t)j;
+        }
+    }
+}
+
 // work items: parts of <= kItemParticles particles of each non-empty z-segment
 __global__ void seg_parts_kernel(const int32_t *__restrict__ cell_start, int n, int seg, int nseg,
                                  int nsegs, int *__restrict__ parts) {
@@ -393,16 +419,21 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
             nz = pz[i];
             if (strengths) ns = strengths[pid[i]];
         }
+        int npi = -1;   // perm entry one chunk ahead of the particle prefetch
+        if (pbeg + kChunk + lane < pend) npi = perm ? perm[pbeg + kChunk + lane] : pbeg + kChunk + lane;
         for (int pos = pbeg; pos < pend; pos += kChunk) {
             const int cnt = min(kChunk, pend - pos);
             const double cx = nx, cy = ny, cz = nz, cs = ns;
-            if (pos + kChunk + lane < pend) {   // prefetch the next chunk
-                const int i = perm ? perm[pos + kChunk + lane] : pos + kChunk + lane;
+            if (npi >= 0) {   // prefetch the next chunk
+                const int i = npi;
                 nx = px[i];
                 ny = py[i];
                 nz = pz[i];
                 if (strengths) ns = strengths[pid[i]];
             }
+            npi = -1;
+            if (pos + 2 * kChunk + lane < pend)
+                npi = perm ? perm[pos + 2 * kChunk + lane] : pos + 2 * kChunk + lane;
             chunk_weights<W, false>(st, tab, poly, lane, cnt, cx, cy, cz, cs, true, h, rh, beta, wc,
                                     wstride, pos + lane);
             int j = 0;
@@ -826,7 +857,9 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
         while (__shfl_sync(kFull, cb, kf - k0 + 1) <= pbeg) ++kf;
         const int64_t yrow = (iy + r) % n;
 
-        // prefetch the first chunk (positions, velocities, id) before the window
+        // prefetch the first chunk (positions, velocities, id) before the window;
+        // the perm entries run one chunk further ahead than the particle data,
+        // so a chunk's data loads never wait on their own perm load
         double nx = 0.0, ny = 0.0, nz = 0.0, nvx = 0.0, nvy = 0.0, nvz = 0.0;
         int64_t nid = 0;
         if (pbeg + lane < pend) {
@@ -835,6 +868,9 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
             if (PUSH) { nvx = P.vx[i]; nvy = P.vy[i]; nvz = P.vz[i]; }
             if (perm || !PUSH || pp.mx) nid = P.id[i];
         }
+        int npi = -1;   // perm entry of this lane's particle in the next chunk
+        if (pbeg + kChunk + lane < pend)
+            npi = perm ? perm[pbeg + kChunk + lane] : pbeg + kChunk + lane;
         // window: slot s = c4 + 4h holds plane z == s (mod 8) of [kf, kf+8)
         double g[8][2][3];
 #pragma unroll
@@ -860,12 +896,15 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                 rank[rank_idx] = rank_val;
                 rank_idx = -1;
             }
-            if (pos + kChunk + lane < pend) {   // prefetch the next chunk
-                const int i = perm ? perm[pos + kChunk + lane] : pos + kChunk + lane;
+            if (npi >= 0) {   // prefetch the next chunk (its perm entry is already here)
+                const int i = npi;
                 nx = P.x[i]; ny = P.y[i]; nz = P.z[i];
                 if (PUSH) { nvx = P.vx[i]; nvy = P.vy[i]; nvz = P.vz[i]; }
                 if (perm || !PUSH || pp.mx) nid = P.id[i];
             }
+            npi = -1;         // and the perm entry of the chunk after it
+            if (pos + 2 * kChunk + lane < pend)
+                npi = perm ? perm[pos + 2 * kChunk + lane] : pos + 2 * kChunk + lane;
             PHASE_MARK(t0);
             WarpChunk &st = wb ? st1 : st0;
             if (wc) {
@@ -932,8 +971,15 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                     const int kk = cell_key(x, y, z, h, pp.rh, pp.w, n);
                     PIF_CHECK(kk >= 0 && kk < n * n * n && i < P.count);
                     key[i] = kk;
-                    rank_val = atomicAdd(&count[kk], 1);
-                    rank_idx = i;
+                    if (rank) {
+                        rank_val = atomicAdd(&count[kk], 1);
+                        rank_idx = i;
+                    } else {
+                        // count only (RED, nothing returns): pif_bin_perm
+                        // assigns the in-cell slots, so no atomic round trip
+                        // sits on this warp's scoreboards
+                        atomicAdd(&count[kk], 1);
+                    }
                 } else {
                     const int64_t o = 3 * id0;
                     E_out[o] = E0;
@@ -1277,7 +1323,8 @@ interp_ring_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                 mirror_store(pp, id, x, y, z, vx, vy, vz);
                 const int kk = cell_key(x, y, z, h, pp.rh, pp.w, n);
                 key[pos] = kk;
-                rank[pos] = atomicAdd(&count[kk], 1);
+                if (rank) rank[pos] = atomicAdd(&count[kk], 1);
+                else atomicAdd(&count[kk], 1);
             } else {
                 const int64_t o = 3 * P.id[i];
                 E_out[o] = E0;
@@ -1373,7 +1420,8 @@ __global__ void interp_generic_kernel(pif_soa_t P, const int32_t *__restrict__ p
             mirror_store(pp, id, x, y, z, vx, vy, vz);
             const int kk = cell_key(x, y, z, pp.h, pp.rh, w, n);
             key[i] = kk;
-            rank[i] = atomicAdd(&count[kk], 1);
+            if (rank) rank[i] = atomicAdd(&count[kk], 1);
+            else atomicAdd(&count[kk], 1);
         } else {
             const int64_t o = 3 * P.id[src];
             E_out[o] = e0;
@@ -1712,11 +1760,18 @@ int launch_bin_perm(Plan &p, const int32_t *key, const int32_t *rank, int64_t M,
         // (the atomic ranks would order a cell's particles by arrival)
         const int rc = det_sort_perm(p, key, M, perm, s);
         if (rc != PIF_OK) return rc;
-    } else if (M > 0) {
+    } else if (M > 0 && rank) {
         bin_perm_kernel<<<grid_for(M, 256, p.sm_count), 256, 0, s>>>(key, rank, p.cell_start, M,
                                                                       perm);
         e = cudaGetLastError();
         if (e != cudaSuccess) return fail_cuda(e, "bin_perm_kernel");
+    } else if (M > 0) {
+        e = cudaMemsetAsync(p.cell_count, 0, sizeof(int32_t) * (p.n3 + 1), s);
+        if (e != cudaSuccess) return fail_cuda(e, "reset cell cursors");
+        bin_perm_cursor_kernel<<<grid_for(M, 256, p.sm_count), 256, 0, s>>>(
+            key, p.cell_count, p.cell_start, M, perm);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return fail_cuda(e, "bin_perm_cursor_kernel");
     }
     const int rc = build_items(p, M, s);
     if (rc != PIF_OK) return rc;

@@ -221,9 +221,10 @@ class PifEngine:
 
     def _bin(self):
         """Cell-ordered view: perm from the keys/ranks of the current buffer."""
-        _native.call("pif_bin_perm", self.handle, self.parts.key.data_ptr(),
-                     self.parts.rank.data_ptr(), self.count, self.parts.perm.data_ptr(),
-                     self._stream())
+        # rank NULL: the in-cell slots come from per-cell cursors in the perm
+        # kernel, so the push never waits on a returning atomic
+        _native.call("pif_bin_perm", self.handle, self.parts.key.data_ptr(), None, self.count,
+                     self.parts.perm.data_ptr(), self._stream())
         # cell scan (CUB: 2 kernels) + perm + work items (segment counts,
         # CUB scan: 2, item table): 7 kernels (profiles/r03_launches.md)
         self.launches += 7
@@ -283,7 +284,7 @@ class PifEngine:
         _native.call("pif_interp_push_perm", self.handle, ctypes.byref(src),
                      self.parts.perm.data_ptr(), ctypes.byref(dst), self.half, self.dt,
                      self._tq, self._sq, self.has_b, self.e_kind, self.parts.key.data_ptr(),
-                     self.parts.rank.data_ptr(), self.diag.data_ptr(), self._stream())
+                     None, self.diag.data_ptr(), self._stream())
         self.parts.swap()
         self.launches += 2
         if self.deterministic:      # the fused sums depend on the work-item schedule
