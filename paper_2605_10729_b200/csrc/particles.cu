@@ -265,6 +265,11 @@ __device__ __forceinline__ void chunk_weights(WarpChunk &st, const double *tab, 
                 st.wx[a][lane] = scale ? __dmul_rn(s, wt[0][a]) : wt[0][a];
                 st.wy[lane][a] = wt[1][a];
                 st.wz[lane][a] = wt[2][a];
+                if (wc) {
+                    wc[a * wstride + wpos] = wt[0][a];
+                    wc[(8 + a) * wstride + wpos] = wt[1][a];
+                    wc[(16 + a) * wstride + wpos] = wt[2][a];
+                }
             }
         } else {
             // wc: also keep the (unscaled) weights for the next gather at these
@@ -378,6 +383,11 @@ constexpr int kSpreadUnroll = PIF_SPREAD_UNROLL;
 #ifndef PIF_SPREAD_MINB
 #define PIF_SPREAD_MINB 4
 #endif
+// 1: the spread evaluates the three axes' weight polynomials interleaved (more
+// ILP, more registers); A/B knob, see DESIGN.md §4
+#ifndef PIF_SPREAD_XYZ
+#define PIF_SPREAD_XYZ 1
+#endif
 
 template <int W, bool DET>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, PIF_SPREAD_MINB)
@@ -446,7 +456,8 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
             npi = -1;
             if (pos + 2 * kChunk + lane < pend)
                 npi = perm ? perm[pos + 2 * kChunk + lane] : pos + 2 * kChunk + lane;
-            chunk_weights<W, false>(st, tab, poly, lane, cnt, cx, cy, cz, cs, true, h, rh, beta, wc,
+            chunk_weights<W, (bool)PIF_SPREAD_XYZ>(st, tab, poly, lane, cnt, cx, cy, cz, cs, true, h,
+                                                  rh, beta, wc,
                                     wstride, pos + lane);
             int j = 0;
             while (j < cnt) {
