@@ -1088,36 +1088,13 @@ __device__ __forceinline__ void tile_load_field(double2 *txy, double *tzc, const
     __syncthreads();
 }
 
-// Warp w of a box walks columns lx = w, ly = 0..7 (64 consecutive cells, keys
-// key0 + 64 w + t) as ONE particle stream, chunked by 32 across column and cell
-// boundaries, so a sparse box still fills the weight / push lanes.  The 65
-// boundaries of those cells are held two per lane.
-struct BoxCells {
-    int lo, hi, end;   // cell_start of cell t (lane t), of cell 32 + t, and of cell 64
-    __device__ __forceinline__ int bound(int t) const {   // warp-uniform t
-        const int a = __shfl_sync(0xffffffffu, lo, t & 31);
-        const int b = __shfl_sync(0xffffffffu, hi, t & 31);
-        return t < 32 ? a : (t < 64 ? b : end);
-    }
-};
-
-__device__ __forceinline__ BoxCells box_cells(const int32_t *cell_start, int key, int lane) {
-    BoxCells c;
-    c.lo = cell_start[key + lane];
-    c.hi = cell_start[key + 32 + lane];
-    c.end = cell_start[key + 64];
-    return c;
-}
-
-// dynamic shared memory of interp_box_kernel: tile (E_x, E_y pairs | E_z), the
-// per-warp partial sums and stages
+// dynamic shared memory of interp_box_kernel: tile (E_x, E_y pairs | E_z) and
+// the per-warp partial sums
 constexpr int kBoxGatherDyn =
     (int)(kBoxPts * (sizeof(double2) + sizeof(double)) +
           kBoxWarps * (sizeof(GatherPartials) + sizeof(WarpChunk)));
-// spread_box_kernel: per warp, the charge of its 8 columns' footprint
-// (8 x-offsets x 15 y x 15 z, plain adds: no other warp writes it) and a stage
-constexpr int kBoxPriv = 8 * kBoxT * kBoxT;
-constexpr int kBoxSpreadDyn = (int)(kBoxWarps * (kBoxPriv * sizeof(double) + sizeof(WarpChunk)));
+// spread_box_kernel: charge tile + the per-warp stages
+constexpr int kBoxSpreadDyn = (int)(kBoxPts * sizeof(double) + kBoxWarps * sizeof(WarpChunk));
 
 template <int W, bool PUSH>
 __global__ void __launch_bounds__(kBoxWarps * 32, 1)
@@ -1133,238 +1110,245 @@ interp_box_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
     GatherPartials &gpart = gps[threadIdx.x >> 5];
     WarpChunk *stage = reinterpret_cast<WarpChunk *>(gps + kBoxWarps);
     __shared__ double tab[32];
-    __shared__ int s_box;
+    __shared__ int s_box, s_col;
     if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    WarpChunk &st = stage[wid];
+    const int lane = threadIdx.x & 31;
+    WarpChunk &st = stage[threadIdx.x >> 5];
     chunk_zero(st, lane);
     const int n = pp.n, nb = n >> 3, nboxes = nb * nb * nb;
     const double h = pp.h;
     const int r = lane >> 2, c4 = lane & 3;
-    const int lx = wid;
     double dg[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     for (;;) {
-        __syncthreads();   // previous box done with the tile and s_box
-        if (threadIdx.x == 0) s_box = (int)atomicAdd(work, 1u);
+        __syncthreads();   // previous box done with the tile and s_box / s_col
+        if (threadIdx.x == 0) {
+            s_box = (int)atomicAdd(work, 1u);
+            s_col = 0;
+        }
         __syncthreads();
         const int box = s_box;
         if (box >= nboxes) break;
         const int key0 = box << 9;
         if (cell_start[key0 + 512] == cell_start[key0]) continue;   // empty box
         const int bz = box % nb, by = (box / nb) % nb, bx = box / (nb * nb);
-        // this warp's cells and first particle chunk, loaded under the tile load
-        const BoxCells cells = box_cells(cell_start, key0 + (lx << 6), lane);
         tile_load_field(txy, tzc, field, n, bx, by, bz);
-        const int pbeg = cells.bound(0), pend = cells.bound(64);
-        if (pbeg == pend) continue;
-        double nx = 0.0, ny = 0.0, nz = 0.0, nvx = 0.0, nvy = 0.0, nvz = 0.0;
-        int64_t nid = 0;
-        if (pbeg + lane < pend) {
-            const int i = perm ? perm[pbeg + lane] : pbeg + lane;
-            nx = P.x[i]; ny = P.y[i]; nz = P.z[i];
-            if (PUSH) { nvx = P.vx[i]; nvy = P.vy[i]; nvz = P.vz[i]; }
-            if (perm || !PUSH || pp.mx) nid = P.id[i];
-        }
-        int t = 0;   // current cell of the walk (ly = t >> 3, lz = t & 7)
-        while (cells.bound(t + 1) <= pbeg) ++t;
-        double g[8][2][3];
-        auto window = [&](int ly, int lz0) {   // slots hold planes lz0 .. lz0 + 7
+        for (;;) {
+            int col = 0;
+            if (lane == 0) col = atomicAdd(&s_col, 1);
+            col = __shfl_sync(kFull, col, 0);
+            if (col >= 64) break;
+            const int lx = col >> 3, ly = col & 7;
+            const int kc = key0 + (col << 3);
+            const int cb = cell_start[kc + min(lane, 8)];   // 9 cell boundaries
+            const int pbeg = __shfl_sync(kFull, cb, 0), pend = __shfl_sync(kFull, cb, 8);
+            if (pbeg == pend) continue;
+            int kf = 0;   // first non-empty cell of the column
+            while (__shfl_sync(kFull, cb, kf + 1) <= pbeg) ++kf;
+            double g[8][2][3];
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
                 const int sl = c4 + 4 * hh;
-                tile_plane(g, hh, txy, tzc, lx, ly + r, lz0 + ((sl - lz0) & 7));
+                tile_plane(g, hh, txy, tzc, lx, ly + r, kf + ((sl - kf) & 7));
             }
-        };
-        window(t >> 3, t & 7);
-        int cell_end = cells.bound(t + 1);
-        for (int pos = pbeg; pos < pend; pos += kChunk) {
-            const int cnt = min(kChunk, pend - pos);
-            const double x0 = nx, y0 = ny, z0 = nz, vx0 = nvx, vy0 = nvy, vz0 = nvz;
-            const int64_t id0 = nid;
-            if (pos + kChunk + lane < pend) {
-                const int i = perm ? perm[pos + kChunk + lane] : pos + kChunk + lane;
+            int k = kf;
+            int cell_end = __shfl_sync(kFull, cb, kf + 1);
+            double nx = 0.0, ny = 0.0, nz = 0.0, nvx = 0.0, nvy = 0.0, nvz = 0.0;
+            int64_t nid = 0;
+            if (pbeg + lane < pend) {
+                const int i = perm ? perm[pbeg + lane] : pbeg + lane;
                 nx = P.x[i]; ny = P.y[i]; nz = P.z[i];
                 if (PUSH) { nvx = P.vx[i]; nvy = P.vy[i]; nvz = P.vz[i]; }
                 if (perm || !PUSH || pp.mx) nid = P.id[i];
             }
-            chunk_weights<W, true>(st, tab, poly, lane, cnt, x0, y0, z0, 1.0, false, h, pp.rh, beta);
-            int j = 0;
-            while (j < cnt) {
-                const int gp = pos + j;
-                if (gp >= cell_end) {
-                    const int k = t & 7;
-                    ++t;
-                    if ((t & 7) == 0) {             // next column: fresh window
-                        while (cells.bound(t + 1) <= gp) ++t;
-                        window(t >> 3, t & 7);
-                    } else {                        // next cell: plane k leaves slot k&7
-                        if (c4 == (k & 3)) {        // compile-time slot index (registers)
-                            if (k >> 2) tile_plane(g, 1, txy, tzc, lx, (t >> 3) + r, k + 8);
-                            else tile_plane(g, 0, txy, tzc, lx, (t >> 3) + r, k + 8);
+            for (int pos = pbeg; pos < pend; pos += kChunk) {
+                const int cnt = min(kChunk, pend - pos);
+                const double x0 = nx, y0 = ny, z0 = nz, vx0 = nvx, vy0 = nvy, vz0 = nvz;
+                const int64_t id0 = nid;
+                if (pos + kChunk + lane < pend) {
+                    const int i = perm ? perm[pos + kChunk + lane] : pos + kChunk + lane;
+                    nx = P.x[i]; ny = P.y[i]; nz = P.z[i];
+                    if (PUSH) { nvx = P.vx[i]; nvy = P.vy[i]; nvz = P.vz[i]; }
+                    if (perm || !PUSH || pp.mx) nid = P.id[i];
+                }
+                chunk_weights<W, true>(st, tab, poly, lane, cnt, x0, y0, z0, 1.0, false, h, pp.rh,
+                                       beta);
+                int j = 0;
+                while (j < cnt) {
+                    const int gp = pos + j;
+                    if (gp >= cell_end) {   // next cell: plane k leaves slot k&7, plane k+8 enters
+                        const int sl = k & 7;
+                        if (c4 == (sl & 3)) {   // compile-time slot index (registers)
+                            if (sl >> 2) tile_plane(g, 1, txy, tzc, lx, ly + r, k + 8);
+                            else tile_plane(g, 0, txy, tzc, lx, ly + r, k + 8);
                         }
+                        ++k;
+                        cell_end = __shfl_sync(kFull, cb, k + 1);
+                        continue;
                     }
-                    cell_end = cells.bound(t + 1);
-                    continue;
+                    const int m = min(8, min(pos + cnt, cell_end) - gp);
+                    if (m <= kGatherFmaMax) gather_sub_fma(st, gpart, g, j, m, k, r, c4);
+                    else gather_sub_d(st, gpart, g, j, m, k, r, c4);
+                    j += m;
                 }
-                const int k = t & 7;
-                const int m = min(8, min(pos + cnt, cell_end) - gp);
-                if (m <= kGatherFmaMax) gather_sub_fma(st, gpart, g, j, m, k, r, c4);
-                else gather_sub_d(st, gpart, g, j, m, k, r, c4);
-                j += m;
-            }
-            __syncwarp();
-            if (lane < cnt) {
-                const int64_t i = pos + lane;
-                double Eg[3];
-                gather_reduce(st, gpart, lane, Eg);
-                if (PUSH) {
-                    double x = x0, y = y0, z = z0, vx = vx0, vy = vy0, vz = vz0;
-                    boris_one(pp, Eg[0], Eg[1], Eg[2], x, y, z, vx, vy, vz, dg);
-                    Q.x[i] = x; Q.y[i] = y; Q.z[i] = z;
-                    Q.vx[i] = vx; Q.vy[i] = vy; Q.vz[i] = vz;
-                    if (perm) Q.id[i] = id0;
-                    mirror_store(pp, id0, x, y, z, vx, vy, vz);
-                    const int kk = cell_key(x, y, z, h, pp.rh, pp.w, n, pp.box);
-                    key[i] = kk;
-                    if (rank) rank[i] = atomicAdd(&count[kk], 1);
-                    else atomicAdd(&count[kk], 1);
-                } else {
-                    const int64_t o = 3 * id0;
-                    E_out[o] = Eg[0];
-                    E_out[o + 1] = Eg[1];
-                    E_out[o + 2] = Eg[2];
+                __syncwarp();
+                if (lane < cnt) {
+                    const int64_t i = pos + lane;
+                    double Eg[3];
+                    gather_reduce(st, gpart, lane, Eg);
+                    if (PUSH) {
+                        double x = x0, y = y0, z = z0, vx = vx0, vy = vy0, vz = vz0;
+                        boris_one(pp, Eg[0], Eg[1], Eg[2], x, y, z, vx, vy, vz, dg);
+                        Q.x[i] = x; Q.y[i] = y; Q.z[i] = z;
+                        Q.vx[i] = vx; Q.vy[i] = vy; Q.vz[i] = vz;
+                        if (perm) Q.id[i] = id0;
+                        mirror_store(pp, id0, x, y, z, vx, vy, vz);
+                        const int kk = cell_key(x, y, z, h, pp.rh, pp.w, n, pp.box);
+                        key[i] = kk;
+                        if (rank) rank[i] = atomicAdd(&count[kk], 1);
+                        else atomicAdd(&count[kk], 1);
+                    } else {
+                        const int64_t o = 3 * id0;
+                        E_out[o] = Eg[0];
+                        E_out[o + 1] = Eg[1];
+                        E_out[o + 2] = Eg[2];
+                    }
                 }
+                __syncwarp();
             }
-            __syncwarp();
         }
     }
     if (PUSH) block_diag_store(dg, partials);
 }
 
+// shared-memory double add (the hardware has no native one: CAS loop)
+__device__ __forceinline__ void smem_add(double *a, double v) { atomicAdd(a, v); }
+
 template <int W>
-__global__ void __launch_bounds__(kBoxWarps * 32, 1)
+__global__ void __launch_bounds__(kBoxWarps * 32, 2)
 spread_box_kernel(const double *__restrict__ px, const double *__restrict__ py,
                   const double *__restrict__ pz, const int64_t *__restrict__ pid,
                   const int32_t *__restrict__ perm, const double *__restrict__ strengths, double q,
                   const int32_t *__restrict__ cell_start, double *__restrict__ grid, int n,
                   double h, double beta, const EsPoly poly, unsigned int *work) {
-    extern __shared__ double dsm[];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    double *priv = dsm + wid * kBoxPriv;   // [a][ty][tz], x = lx + a
-    WarpChunk &st = reinterpret_cast<WarpChunk *>(dsm + kBoxWarps * kBoxPriv)[wid];
+    extern __shared__ double dtile[];     // kBoxPts charge accumulators | per-warp stages
+    WarpChunk *stage = reinterpret_cast<WarpChunk *>(dtile + kBoxPts);
     __shared__ double tab[32];
-    __shared__ int s_box;
+    __shared__ int s_box, s_col;
     if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
     const double rh = __drcp_rn(h);
+    const int lane = threadIdx.x & 31;
+    WarpChunk &st = stage[threadIdx.x >> 5];
     chunk_zero(st, lane);
-    for (int i = lane; i < kBoxPriv; i += 32) priv[i] = 0.0;
     const int nb = n >> 3, nboxes = nb * nb * nb;
     const int r = lane >> 2, c4 = lane & 3;
-    const int lx = wid;
+    for (int t = threadIdx.x; t < kBoxPts; t += blockDim.x) dtile[t] = 0.0;
     for (;;) {
         __syncthreads();
-        if (threadIdx.x == 0) s_box = (int)atomicAdd(work, 1u);
+        if (threadIdx.x == 0) {
+            s_box = (int)atomicAdd(work, 1u);
+            s_col = 0;
+        }
         __syncthreads();
         const int box = s_box;
         if (box >= nboxes) break;
         const int key0 = box << 9;
-        const BoxCells cells = box_cells(cell_start, key0 + (lx << 6), lane);
-        const int pbeg = cells.bound(0), pend = cells.bound(64);
-        if (pbeg == pend) continue;
+        if (cell_start[key0 + 512] == cell_start[key0]) continue;
         const int bz = box % nb, by = (box / nb) % nb, bx = box / (nb * nb);
-        double acc[8][2];
+        for (;;) {
+            int col = 0;
+            if (lane == 0) col = atomicAdd(&s_col, 1);
+            col = __shfl_sync(kFull, col, 0);
+            if (col >= 64) break;
+            const int lx = col >> 3, ly = col & 7;
+            const int kc = key0 + (col << 3);
+            const int cb = cell_start[kc + min(lane, 8)];
+            const int pbeg = __shfl_sync(kFull, cb, 0), pend = __shfl_sync(kFull, cb, 8);
+            if (pbeg == pend) continue;
+            int k = 0;
+            while (__shfl_sync(kFull, cb, k + 1) <= pbeg) ++k;
+            int cell_end = __shfl_sync(kFull, cb, k + 1);
+            double acc[8][2];
 #pragma unroll
-        for (int a = 0; a < 8; ++a) acc[a][0] = acc[a][1] = 0.0;
-        // plane tz of column ly (this lane's row b = r) into the private buffer
-        auto flush = [&](int ly, int tz) {
-            const int sl = tz & 7;
-            if (c4 == (sl >> 1)) {
-                const int jj = sl & 1;
-                double *row = priv + (ly + r) * kBoxT + tz;
+            for (int a = 0; a < 8; ++a) acc[a][0] = acc[a][1] = 0.0;
+            // flush slot (plane tz) of this lane's row b = r into the tile
+            auto flush = [&](int tz) {
+                const int sl = tz & 7;
+                if (c4 == (sl >> 1)) {
+                    const int jj = sl & 1;
 #pragma unroll
-                for (int a = 0; a < W; ++a) row[a * kBoxT * kBoxT] += jj ? acc[a][1] : acc[a][0];
+                    for (int a = 0; a < W; ++a) {
+                        const double v = jj ? acc[a][1] : acc[a][0];
+                        if (v != 0.0) smem_add(&dtile[box_pt(lx + a, ly + r, tz)], v);
+                    }
 #pragma unroll
-                for (int a = 0; a < 8; ++a) {
-                    if (jj) acc[a][1] = 0.0;
-                    else acc[a][0] = 0.0;
+                    for (int a = 0; a < 8; ++a) {
+                        if (jj) acc[a][1] = 0.0;
+                        else acc[a][0] = 0.0;
+                    }
                 }
-            }
-        };
-        double nx = 0.0, ny = 0.0, nz = 0.0, ns = q;
-        if (pbeg + lane < pend) {
-            const int i = perm ? perm[pbeg + lane] : pbeg + lane;
-            nx = px[i]; ny = py[i]; nz = pz[i];
-            if (strengths) ns = strengths[pid[i]];
-        }
-        int t = 0;
-        while (cells.bound(t + 1) <= pbeg) ++t;
-        int cell_end = cells.bound(t + 1);
-        for (int pos = pbeg; pos < pend; pos += kChunk) {
-            const int cnt = min(kChunk, pend - pos);
-            const double cx = nx, cy = ny, cz = nz, cs = ns;
-            if (pos + kChunk + lane < pend) {
-                const int i = perm ? perm[pos + kChunk + lane] : pos + kChunk + lane;
+            };
+            double nx = 0.0, ny = 0.0, nz = 0.0, ns = q;
+            if (pbeg + lane < pend) {
+                const int i = perm ? perm[pbeg + lane] : pbeg + lane;
                 nx = px[i]; ny = py[i]; nz = pz[i];
                 if (strengths) ns = strengths[pid[i]];
             }
-            chunk_weights<W, false>(st, tab, poly, lane, cnt, cx, cy, cz, cs, true, h, rh, beta);
-            int j = 0;
-            while (j < cnt) {
-                if (pos + j >= cell_end) {
-                    const int ly = t >> 3, k = t & 7;
-                    ++t;
-                    if ((t & 7) == 0) {             // column done: its 8 pending planes
-#pragma unroll 1
-                        for (int u = 0; u < 8; ++u) flush(ly, k + u);
-                    } else {
-                        flush(ly, k);
+            for (int pos = pbeg; pos < pend; pos += kChunk) {
+                const int cnt = min(kChunk, pend - pos);
+                const double cx = nx, cy = ny, cz = nz, cs = ns;
+                if (pos + kChunk + lane < pend) {
+                    const int i = perm ? perm[pos + kChunk + lane] : pos + kChunk + lane;
+                    nx = px[i]; ny = py[i]; nz = pz[i];
+                    if (strengths) ns = strengths[pid[i]];
+                }
+                chunk_weights<W, false>(st, tab, poly, lane, cnt, cx, cy, cz, cs, true, h, rh, beta);
+                int j = 0;
+                while (j < cnt) {
+                    if (pos + j >= cell_end) {
+                        flush(k);
+                        ++k;
+                        cell_end = __shfl_sync(kFull, cb, k + 1);
+                        continue;
                     }
-                    cell_end = cells.bound(t + 1);
-                    continue;
-                }
-                const int jend = min(cnt, cell_end - pos);
-                const int zs = (r - (t & 7)) & 7;
-                for (; j + 4 <= jend; j += 4) {
-                    const int pj = j + c4;
-                    const double wyb = st.wy[pj][r];
-                    const double bz0 = st.wz[pj][zs];
+                    const int jend = min(cnt, cell_end - pos);
+                    const int zs = (r - k) & 7;
+                    for (; j + 4 <= jend; j += 4) {
+                        const int pj = j + c4;
+                        const double wyb = st.wy[pj][r];
+                        const double bz0 = st.wz[pj][zs];
 #pragma unroll
-                    for (int a = 0; a < 8; ++a)
-                        dmma884(acc[a][0], acc[a][1], st.wx[a][pj] * wyb, bz0);
-                }
-                if (j < jend) {
-                    const bool ok = c4 < jend - j;
-                    const int pj = ok ? j + c4 : j;
-                    const double wyb = ok ? st.wy[pj][r] : 0.0;
-                    const double bz0 = st.wz[pj][zs];
+                        for (int a = 0; a < 8; ++a)
+                            dmma884(acc[a][0], acc[a][1], st.wx[a][pj] * wyb, bz0);
+                    }
+                    if (j < jend) {
+                        const bool ok = c4 < jend - j;
+                        const int pj = ok ? j + c4 : j;
+                        const double wyb = ok ? st.wy[pj][r] : 0.0;
+                        const double bz0 = st.wz[pj][zs];
 #pragma unroll
-                    for (int a = 0; a < 8; ++a)
-                        dmma884(acc[a][0], acc[a][1], st.wx[a][pj] * wyb, bz0);
-                    j = jend;
+                        for (int a = 0; a < 8; ++a)
+                            dmma884(acc[a][0], acc[a][1], st.wx[a][pj] * wyb, bz0);
+                        j = jend;
+                    }
                 }
+                __syncwarp();
             }
-            __syncwarp();
+            // the remaining planes of the column: tz = k .. k + 7 (slot order)
+            for (int t = 0; t < 8; ++t) flush(k + t);
         }
-        {   // the last column's pending planes
-            const int ly = t >> 3, k = t & 7;
-#pragma unroll 1
-            for (int u = 0; u < 8; ++u) flush(ly, k + u);
-        }
-        __syncwarp();
-        // this warp's footprint charge -> grid (one REDG per nonzero point)
-        for (int i = lane; i < kBoxPriv; i += 32) {
-            const double v = priv[i];
+        __syncthreads();   // every column of the box flushed into the tile
+        for (int t = threadIdx.x; t < kBoxPts; t += blockDim.x) {
+            const double v = dtile[t];
             if (v != 0.0) {
-                const int tz = i % kBoxT, ty = (i / kBoxT) % kBoxT, a = i / (kBoxT * kBoxT);
-                int X = 8 * bx + lx + a, Y = 8 * by + ty, Z = 8 * bz + tz;
+                const int tz = t % kBoxT, ty = (t / kBoxT) % kBoxT, tx = t / (kBoxT * kBoxT);
+                int X = 8 * bx + tx, Y = 8 * by + ty, Z = 8 * bz + tz;
                 X = X >= n ? X - n : X;
                 Y = Y >= n ? Y - n : Y;
                 Z = Z >= n ? Z - n : Z;
                 atomicAdd(grid + ((int64_t)X * n + Y) * n + Z, v);
-                priv[i] = 0.0;
+                dtile[t] = 0.0;
             }
         }
-        __syncwarp();
     }
 }
 

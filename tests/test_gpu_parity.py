@@ -382,11 +382,6 @@ def big(cuda):
     return dict(torch=torch, spec=spec, plan=plan, x=x, v=v, ids=ids, eng=eng, q=q, m=m)
 
 
-def _native_layout(eng):
-    from paper_2605_10729_b200 import _native
-    return _native.load().pif_key_layout(eng.handle)
-
-
 def test_binning_sorts_by_stencil_cell(big):
     torch = big["torch"]
     eng, plan = big["eng"], big["plan"]
@@ -398,12 +393,7 @@ def test_binning_sorts_by_stencil_cell(big):
     for d in range(3):
         c = soa[d] / h
         keys.append(torch.remainder(torch.ceil(c - 0.5 * w).long(), n))
-    if _native_layout(eng):     # 8^3-box key order (sparse sets, particles.cu key_of)
-        nb = n // 8
-        box = ((keys[0] // 8) * nb + keys[1] // 8) * nb + keys[2] // 8
-        key = box * 512 + ((keys[0] % 8) * 8 + keys[1] % 8) * 8 + keys[2] % 8
-    else:
-        key = (keys[0] * n + keys[1]) * n + keys[2]
+    key = (keys[0] * n + keys[1]) * n + keys[2]
     assert bool((key[1:] >= key[:-1]).all())
     assert torch.equal(torch.sort(eng.parts.ids[eng.parts.cur][:eng.count])[0], big["ids"])
 
