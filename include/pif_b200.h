@@ -237,13 +237,6 @@ int pif_probe_fp64(double *scratch, int blocks, int threads, int iters, void *st
  * the push.  Same results to rounding as the default mode, identical bits run
  * to run.  Only for the DMMA kernels (w <= 8); PIF_ERR_VALUE otherwise. */
 int pif_set_deterministic(pif_plan_t plan, int enable);
-/* Key layout of the plan's particle set, fixed by its first binning
- * (pif_bin_keys / pif_load_aos): 0 = columns ((kx*n + ky)*n + kz; the column
- * kernels), 1 = 8^3-cell boxes (sparse sets below ~12 particles per stencil
- * cell with n % 8 == 0 and w <= 8; the box kernels, one CTA per box with its
- * field / charge tile in shared memory).  Env PIF_BOX=0/1 at plan creation
- * forces it where allowed. */
-int pif_key_layout(pif_plan_t plan);
 int pif_is_deterministic(pif_plan_t plan);
 
 /* ---- in-process communicators: replaces comm.allreduce_sum's fixed-order

@@ -210,7 +210,6 @@ int pif_plan_create(const pif_plan_desc_t *d, int device, pif_plan_t *out) {
     if (const char *fg = std::getenv("PIF_FORCE_GENERIC")) p.force_generic = std::atoi(fg) != 0;
     if (const char *st = std::getenv("PIF_SEG_TARGET")) p.seg_target = std::max(1, std::atoi(st));
     if (const char *fr = std::getenv("PIF_FORCE_RING")) p.force_ring = std::atoi(fr) != 0;
-    if (const char *bx = std::getenv("PIF_BOX")) p.box_force = std::atoi(bx) != 0 ? 1 : 0;
     int rc = PIF_OK;
 #define TRY(x)                    \
     do {                          \
@@ -403,16 +402,12 @@ int pif_set_deterministic(pif_plan_t plan, int enable) {
     if (enable && !pif::det_supported(p))
         return pif::bad("deterministic mode covers the DMMA kernels only: window width w <= 8 "
                         "(eps >= 1e-7)");
-    if (enable && p.box)
-        return pif::bad("enable deterministic mode before the particles are binned");
     p.det = enable != 0;
     if (p.det) p.wcache_valid = false;
     return PIF_OK;
 }
 
 int pif_is_deterministic(pif_plan_t plan) { return plan && plan->p.det ? 1 : 0; }
-
-int pif_key_layout(pif_plan_t plan) { return plan && plan->p.box ? 1 : 0; }
 
 int pif_fft_timing(pif_plan_t plan, int slots) {
     if (!plan) return pif::bad("null plan");

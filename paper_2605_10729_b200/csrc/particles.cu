@@ -31,24 +31,12 @@ __device__ __forceinline__ int cell_index_of(double c, int w, int n) {
     return pmod((int)stencil_start(c, w), n);
 }
 
-// Cell key of a particle: its ES-stencil start cell (kx, ky, kz).  Column
-// layout (box == 0): (kx * n + ky) * n + kz, so a z-column of cells is
-// contiguous.  Box layout (box == 1, sparse sets, n % 8 == 0): boxes of 8^3
-// cells in (bx, by, bz) order, cells inside a box in (lx, ly, lz) order, so a
-// box is contiguous and each of its 64 z-columns of 8 cells too.
-__device__ __forceinline__ int key_of(int kx, int ky, int kz, int n, int box) {
-    if (!box) return (kx * n + ky) * n + kz;
-    const int nb = n >> 3;
-    return ((((kx >> 3) * nb + (ky >> 3)) * nb + (kz >> 3)) << 9) | ((kx & 7) << 6) |
-           ((ky & 7) << 3) | (kz & 7);
-}
-
 __device__ __forceinline__ int cell_key(double x, double y, double z, double h, double rh, int w,
-                                        int n, int box = 0) {
+                                        int n) {
     int kx = cell_index_of(axis_coord(x, h, rh), w, n);
     int ky = cell_index_of(axis_coord(y, h, rh), w, n);
     int kz = cell_index_of(axis_coord(z, h, rh), w, n);
-    return key_of(kx, ky, kz, n, box);
+    return (kx * n + ky) * n + kz;
 }
 
 // ----------------------------------------------------------------------------
@@ -66,12 +54,12 @@ __global__ void wrap_kernel(double *x, double *y, double *z, int64_t M, double L
 
 __global__ void bin_keys_kernel(const double *__restrict__ x, const double *__restrict__ y,
                                 const double *__restrict__ z, int64_t M, double h, int w, int n,
-                                int box, int32_t *__restrict__ key, int32_t *__restrict__ rank,
+                                int32_t *__restrict__ key, int32_t *__restrict__ rank,
                                 int32_t *__restrict__ count) {
     const double rh = __drcp_rn(h);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M;
          i += (int64_t)gridDim.x * blockDim.x) {
-        int k = cell_key(x[i], y[i], z[i], h, rh, w, n, box);
+        int k = cell_key(x[i], y[i], z[i], h, rh, w, n);
         key[i] = k;
         rank[i] = atomicAdd(&count[k], 1);
     }
@@ -120,7 +108,7 @@ __global__ void soa_to_aos_by_id_kernel(pif_soa_t P, int64_t id0, double *__rest
 // order -> wrapped SoA store, ids id0 + i, cell keys and ranks.
 __global__ void load_aos_kernel(const double *__restrict__ xa, const double *__restrict__ va,
                                 int64_t id0, int64_t M, pif_soa_t dst, double L, double h,
-                                int w, int n, int box, int32_t *__restrict__ key,
+                                int w, int n, int32_t *__restrict__ key,
                                 int32_t *__restrict__ rank, int32_t *__restrict__ count) {
     const double rh = __drcp_rn(h);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M;
@@ -134,7 +122,7 @@ __global__ void load_aos_kernel(const double *__restrict__ xa, const double *__r
         dst.vy[i] = va[3 * i + 1];
         dst.vz[i] = va[3 * i + 2];
         dst.id[i] = id0 + i;
-        const int k = cell_key(x, y, z, h, rh, w, n, box);
+        const int k = cell_key(x, y, z, h, rh, w, n);
         key[i] = k;
         rank[i] = atomicAdd(&count[k], 1);
     }
@@ -570,7 +558,6 @@ struct PushParams {
     double ext_c, ext_xy, ext_z, pot_xy, pot_z;   // L/2, -15/L, 30/L, 7.5/L, 15/L
     double tq[3], sq[3];
     int has_b, e_kind, n, w;
-    int box;              // key layout of the next binning (key_of)
     double *mx, *mv;      // id-order mirror (pif_set_id_order_output) or null
     long long mid0;
 };
@@ -992,7 +979,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                     Q.vx[i] = vx; Q.vy[i] = vy; Q.vz[i] = vz;
                     if (perm) Q.id[i] = id0;
                     mirror_store(pp, id0, x, y, z, vx, vy, vz);
-                    const int kk = cell_key(x, y, z, h, pp.rh, pp.w, n, pp.box);
+                    const int kk = cell_key(x, y, z, h, pp.rh, pp.w, n);
                     PIF_CHECK(kk >= 0 && kk < n * n * n && i < P.count);
                     key[i] = kk;
                     if (rank) {
@@ -1028,328 +1015,6 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
     prefetch_wait();
     if (PUSH && rank_idx >= 0) rank[rank_idx] = rank_val;
     if (PUSH) block_diag_store(dg, partials);
-}
-
-// ----------------------------------------------------------------------------
-// sparse sets (box mode): one CTA per 8^3-cell box, field / charge tile in
-// shared memory
-//
-// At a few particles per stencil cell the column kernels above spend their
-// time on plane traffic: every cell step of a column walk brings (gather) or
-// flushes (spread) a whole 8 x 8 plane for ~1 particle, and neighbouring
-// columns fetch the same planes again from L2/HBM.  With cell keys in box
-// order (key_of, box == 1) a box's particles are contiguous and so is each of
-// its 64 columns of 8 cells.  The CTA stages the box's whole footprint once,
-// (8 + 7)^3 points, and its warps walk the box's columns exactly like the
-// column kernels, with the register window fed from (gather) or flushed into
-// (spread) the shared tile.  Per box that is one tile load (gather: 81 KB of
-// E) or one tile flush (spread: <= 3375 REDG) instead of 64 x 15 plane loads or
-// flushes.
-// ----------------------------------------------------------------------------
-
-constexpr int kBoxWarps = 8;
-constexpr int kBoxT = 15;                       // tile edge: 8 cells + 7 (w <= 8)
-constexpr int kBoxPts = kBoxT * kBoxT * kBoxT;  // 3375
-
-__device__ __forceinline__ int box_pt(int tx, int ty, int tz) { return (tx * kBoxT + ty) * kBoxT + tz; }
-
-// window slot hh <- plane tz of the tile for this lane's row b = r
-__device__ __forceinline__ void tile_plane(double (&g)[8][2][3], int hh, const double2 *txy,
-                                           const double *tzc, int lx, int ly, int tz) {
-#pragma unroll
-    for (int a = 0; a < 8; ++a) {
-        const int q = box_pt(lx + a, ly, tz);
-        const double2 v = txy[q];
-        g[a][hh][0] = v.x;
-        g[a][hh][1] = v.y;
-        g[a][hh][2] = tzc[q];
-    }
-}
-
-// Field tile of box (bx, by, bz): points (8bx + tx, 8by + ty, 8bz + tz) mod n,
-// t* in [0, 15), into (Ex, Ey) pairs and Ez with cp.async (LDGSTS).
-__device__ __forceinline__ void tile_load_field(double2 *txy, double *tzc, const double4 *field,
-                                                int n, int bx, int by, int bz) {
-    for (int t = threadIdx.x; t < kBoxPts; t += blockDim.x) {
-        const int tz = t % kBoxT, ty = (t / kBoxT) % kBoxT, tx = t / (kBoxT * kBoxT);
-        int X = 8 * bx + tx, Y = 8 * by + ty, Z = 8 * bz + tz;
-        X = X >= n ? X - n : X;
-        Y = Y >= n ? Y - n : Y;
-        Z = Z >= n ? Z - n : Z;
-        const double4 *src = field + ((int64_t)X * n + Y) * n + Z;
-        const unsigned dxy = (unsigned)__cvta_generic_to_shared(txy + t);
-        const unsigned dz = (unsigned)__cvta_generic_to_shared(tzc + t);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dxy), "l"(src));
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dz),
-                     "l"(reinterpret_cast<const double *>(src) + 2));
-    }
-    asm volatile("cp.async.commit_group;");
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncthreads();
-}
-
-// dynamic shared memory of interp_box_kernel: tile (E_x, E_y pairs | E_z) and
-// the per-warp partial sums
-constexpr int kBoxGatherDyn =
-    (int)(kBoxPts * (sizeof(double2) + sizeof(double)) +
-          kBoxWarps * (sizeof(GatherPartials) + sizeof(WarpChunk)));
-// spread_box_kernel: charge tile + the per-warp stages
-constexpr int kBoxSpreadDyn = (int)(kBoxPts * sizeof(double) + kBoxWarps * sizeof(WarpChunk));
-
-template <int W, bool PUSH>
-__global__ void __launch_bounds__(kBoxWarps * 32, 1)
-interp_box_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
-                  const int32_t *__restrict__ cell_start, const double4 *__restrict__ field,
-                  double beta, const EsPoly poly, PushParams pp, int32_t *__restrict__ key,
-                  int32_t *__restrict__ rank, int32_t *__restrict__ count,
-                  double *__restrict__ partials, double *__restrict__ E_out, unsigned int *work) {
-    extern __shared__ double4 dyn_smem[];
-    double2 *txy = reinterpret_cast<double2 *>(dyn_smem);
-    double *tzc = reinterpret_cast<double *>(txy + kBoxPts);
-    GatherPartials *gps = reinterpret_cast<GatherPartials *>(tzc + kBoxPts);
-    GatherPartials &gpart = gps[threadIdx.x >> 5];
-    WarpChunk *stage = reinterpret_cast<WarpChunk *>(gps + kBoxWarps);
-    __shared__ double tab[32];
-    __shared__ int s_box, s_col;
-    if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
-    const int lane = threadIdx.x & 31;
-    WarpChunk &st = stage[threadIdx.x >> 5];
-    chunk_zero(st, lane);
-    const int n = pp.n, nb = n >> 3, nboxes = nb * nb * nb;
-    const double h = pp.h;
-    const int r = lane >> 2, c4 = lane & 3;
-    double dg[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    for (;;) {
-        __syncthreads();   // previous box done with the tile and s_box / s_col
-        if (threadIdx.x == 0) {
-            s_box = (int)atomicAdd(work, 1u);
-            s_col = 0;
-        }
-        __syncthreads();
-        const int box = s_box;
-        if (box >= nboxes) break;
-        const int key0 = box << 9;
-        if (cell_start[key0 + 512] == cell_start[key0]) continue;   // empty box
-        const int bz = box % nb, by = (box / nb) % nb, bx = box / (nb * nb);
-        tile_load_field(txy, tzc, field, n, bx, by, bz);
-        for (;;) {
-            int col = 0;
-            if (lane == 0) col = atomicAdd(&s_col, 1);
-            col = __shfl_sync(kFull, col, 0);
-            if (col >= 64) break;
-            const int lx = col >> 3, ly = col & 7;
-            const int kc = key0 + (col << 3);
-            const int cb = cell_start[kc + min(lane, 8)];   // 9 cell boundaries
-            const int pbeg = __shfl_sync(kFull, cb, 0), pend = __shfl_sync(kFull, cb, 8);
-            if (pbeg == pend) continue;
-            int kf = 0;   // first non-empty cell of the column
-            while (__shfl_sync(kFull, cb, kf + 1) <= pbeg) ++kf;
-            double g[8][2][3];
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                const int sl = c4 + 4 * hh;
-                tile_plane(g, hh, txy, tzc, lx, ly + r, kf + ((sl - kf) & 7));
-            }
-            int k = kf;
-            int cell_end = __shfl_sync(kFull, cb, kf + 1);
-            double nx = 0.0, ny = 0.0, nz = 0.0, nvx = 0.0, nvy = 0.0, nvz = 0.0;
-            int64_t nid = 0;
-            if (pbeg + lane < pend) {
-                const int i = perm ? perm[pbeg + lane] : pbeg + lane;
-                nx = P.x[i]; ny = P.y[i]; nz = P.z[i];
-                if (PUSH) { nvx = P.vx[i]; nvy = P.vy[i]; nvz = P.vz[i]; }
-                if (perm || !PUSH || pp.mx) nid = P.id[i];
-            }
-            for (int pos = pbeg; pos < pend; pos += kChunk) {
-                const int cnt = min(kChunk, pend - pos);
-                const double x0 = nx, y0 = ny, z0 = nz, vx0 = nvx, vy0 = nvy, vz0 = nvz;
-                const int64_t id0 = nid;
-                if (pos + kChunk + lane < pend) {
-                    const int i = perm ? perm[pos + kChunk + lane] : pos + kChunk + lane;
-                    nx = P.x[i]; ny = P.y[i]; nz = P.z[i];
-                    if (PUSH) { nvx = P.vx[i]; nvy = P.vy[i]; nvz = P.vz[i]; }
-                    if (perm || !PUSH || pp.mx) nid = P.id[i];
-                }
-                chunk_weights<W, true>(st, tab, poly, lane, cnt, x0, y0, z0, 1.0, false, h, pp.rh,
-                                       beta);
-                int j = 0;
-                while (j < cnt) {
-                    const int gp = pos + j;
-                    if (gp >= cell_end) {   // next cell: plane k leaves slot k&7, plane k+8 enters
-                        const int sl = k & 7;
-                        if (c4 == (sl & 3)) {   // compile-time slot index (registers)
-                            if (sl >> 2) tile_plane(g, 1, txy, tzc, lx, ly + r, k + 8);
-                            else tile_plane(g, 0, txy, tzc, lx, ly + r, k + 8);
-                        }
-                        ++k;
-                        cell_end = __shfl_sync(kFull, cb, k + 1);
-                        continue;
-                    }
-                    const int m = min(8, min(pos + cnt, cell_end) - gp);
-                    if (m <= kGatherFmaMax) gather_sub_fma(st, gpart, g, j, m, k, r, c4);
-                    else gather_sub_d(st, gpart, g, j, m, k, r, c4);
-                    j += m;
-                }
-                __syncwarp();
-                if (lane < cnt) {
-                    const int64_t i = pos + lane;
-                    double Eg[3];
-                    gather_reduce(st, gpart, lane, Eg);
-                    if (PUSH) {
-                        double x = x0, y = y0, z = z0, vx = vx0, vy = vy0, vz = vz0;
-                        boris_one(pp, Eg[0], Eg[1], Eg[2], x, y, z, vx, vy, vz, dg);
-                        Q.x[i] = x; Q.y[i] = y; Q.z[i] = z;
-                        Q.vx[i] = vx; Q.vy[i] = vy; Q.vz[i] = vz;
-                        if (perm) Q.id[i] = id0;
-                        mirror_store(pp, id0, x, y, z, vx, vy, vz);
-                        const int kk = cell_key(x, y, z, h, pp.rh, pp.w, n, pp.box);
-                        key[i] = kk;
-                        if (rank) rank[i] = atomicAdd(&count[kk], 1);
-                        else atomicAdd(&count[kk], 1);
-                    } else {
-                        const int64_t o = 3 * id0;
-                        E_out[o] = Eg[0];
-                        E_out[o + 1] = Eg[1];
-                        E_out[o + 2] = Eg[2];
-                    }
-                }
-                __syncwarp();
-            }
-        }
-    }
-    if (PUSH) block_diag_store(dg, partials);
-}
-
-// shared-memory double add (the hardware has no native one: CAS loop)
-__device__ __forceinline__ void smem_add(double *a, double v) { atomicAdd(a, v); }
-
-template <int W>
-__global__ void __launch_bounds__(kBoxWarps * 32, 2)
-spread_box_kernel(const double *__restrict__ px, const double *__restrict__ py,
-                  const double *__restrict__ pz, const int64_t *__restrict__ pid,
-                  const int32_t *__restrict__ perm, const double *__restrict__ strengths, double q,
-                  const int32_t *__restrict__ cell_start, double *__restrict__ grid, int n,
-                  double h, double beta, const EsPoly poly, unsigned int *work) {
-    extern __shared__ double dtile[];     // kBoxPts charge accumulators | per-warp stages
-    WarpChunk *stage = reinterpret_cast<WarpChunk *>(dtile + kBoxPts);
-    __shared__ double tab[32];
-    __shared__ int s_box, s_col;
-    if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
-    const double rh = __drcp_rn(h);
-    const int lane = threadIdx.x & 31;
-    WarpChunk &st = stage[threadIdx.x >> 5];
-    chunk_zero(st, lane);
-    const int nb = n >> 3, nboxes = nb * nb * nb;
-    const int r = lane >> 2, c4 = lane & 3;
-    for (int t = threadIdx.x; t < kBoxPts; t += blockDim.x) dtile[t] = 0.0;
-    for (;;) {
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            s_box = (int)atomicAdd(work, 1u);
-            s_col = 0;
-        }
-        __syncthreads();
-        const int box = s_box;
-        if (box >= nboxes) break;
-        const int key0 = box << 9;
-        if (cell_start[key0 + 512] == cell_start[key0]) continue;
-        const int bz = box % nb, by = (box / nb) % nb, bx = box / (nb * nb);
-        for (;;) {
-            int col = 0;
-            if (lane == 0) col = atomicAdd(&s_col, 1);
-            col = __shfl_sync(kFull, col, 0);
-            if (col >= 64) break;
-            const int lx = col >> 3, ly = col & 7;
-            const int kc = key0 + (col << 3);
-            const int cb = cell_start[kc + min(lane, 8)];
-            const int pbeg = __shfl_sync(kFull, cb, 0), pend = __shfl_sync(kFull, cb, 8);
-            if (pbeg == pend) continue;
-            int k = 0;
-            while (__shfl_sync(kFull, cb, k + 1) <= pbeg) ++k;
-            int cell_end = __shfl_sync(kFull, cb, k + 1);
-            double acc[8][2];
-#pragma unroll
-            for (int a = 0; a < 8; ++a) acc[a][0] = acc[a][1] = 0.0;
-            // flush slot (plane tz) of this lane's row b = r into the tile
-            auto flush = [&](int tz) {
-                const int sl = tz & 7;
-                if (c4 == (sl >> 1)) {
-                    const int jj = sl & 1;
-#pragma unroll
-                    for (int a = 0; a < W; ++a) {
-                        const double v = jj ? acc[a][1] : acc[a][0];
-                        if (v != 0.0) smem_add(&dtile[box_pt(lx + a, ly + r, tz)], v);
-                    }
-#pragma unroll
-                    for (int a = 0; a < 8; ++a) {
-                        if (jj) acc[a][1] = 0.0;
-                        else acc[a][0] = 0.0;
-                    }
-                }
-            };
-            double nx = 0.0, ny = 0.0, nz = 0.0, ns = q;
-            if (pbeg + lane < pend) {
-                const int i = perm ? perm[pbeg + lane] : pbeg + lane;
-                nx = px[i]; ny = py[i]; nz = pz[i];
-                if (strengths) ns = strengths[pid[i]];
-            }
-            for (int pos = pbeg; pos < pend; pos += kChunk) {
-                const int cnt = min(kChunk, pend - pos);
-                const double cx = nx, cy = ny, cz = nz, cs = ns;
-                if (pos + kChunk + lane < pend) {
-                    const int i = perm ? perm[pos + kChunk + lane] : pos + kChunk + lane;
-                    nx = px[i]; ny = py[i]; nz = pz[i];
-                    if (strengths) ns = strengths[pid[i]];
-                }
-                chunk_weights<W, false>(st, tab, poly, lane, cnt, cx, cy, cz, cs, true, h, rh, beta);
-                int j = 0;
-                while (j < cnt) {
-                    if (pos + j >= cell_end) {
-                        flush(k);
-                        ++k;
-                        cell_end = __shfl_sync(kFull, cb, k + 1);
-                        continue;
-                    }
-                    const int jend = min(cnt, cell_end - pos);
-                    const int zs = (r - k) & 7;
-                    for (; j + 4 <= jend; j += 4) {
-                        const int pj = j + c4;
-                        const double wyb = st.wy[pj][r];
-                        const double bz0 = st.wz[pj][zs];
-#pragma unroll
-                        for (int a = 0; a < 8; ++a)
-                            dmma884(acc[a][0], acc[a][1], st.wx[a][pj] * wyb, bz0);
-                    }
-                    if (j < jend) {
-                        const bool ok = c4 < jend - j;
-                        const int pj = ok ? j + c4 : j;
-                        const double wyb = ok ? st.wy[pj][r] : 0.0;
-                        const double bz0 = st.wz[pj][zs];
-#pragma unroll
-                        for (int a = 0; a < 8; ++a)
-                            dmma884(acc[a][0], acc[a][1], st.wx[a][pj] * wyb, bz0);
-                        j = jend;
-                    }
-                }
-                __syncwarp();
-            }
-            // the remaining planes of the column: tz = k .. k + 7 (slot order)
-            for (int t = 0; t < 8; ++t) flush(k + t);
-        }
-        __syncthreads();   // every column of the box flushed into the tile
-        for (int t = threadIdx.x; t < kBoxPts; t += blockDim.x) {
-            const double v = dtile[t];
-            if (v != 0.0) {
-                const int tz = t % kBoxT, ty = (t / kBoxT) % kBoxT, tx = t / (kBoxT * kBoxT);
-                int X = 8 * bx + tx, Y = 8 * by + ty, Z = 8 * bz + tz;
-                X = X >= n ? X - n : X;
-                Y = Y >= n ? Y - n : Y;
-                Z = Z >= n ? Z - n : Z;
-                atomicAdd(grid + ((int64_t)X * n + Y) * n + Z, v);
-                dtile[t] = 0.0;
-            }
-        }
-    }
 }
 
 // ----------------------------------------------------------------------------
@@ -1935,7 +1600,6 @@ PushParams make_push(const Plan &p, double half, double dt, const double *tq, co
     pp.e_kind = e_kind;
     pp.n = p.n;
     pp.w = p.w;
-    pp.box = p.box ? 1 : 0;
     pp.mx = p.mirror_x;
     pp.mv = p.mirror_v;
     pp.mid0 = p.mirror_id0;
@@ -1957,24 +1621,10 @@ int launch_wrap(Plan &p, double *x, double *y, double *z, int64_t M, cudaStream_
     return fail_cuda(cudaGetLastError(), "wrap_kernel");
 }
 
-// Key layout for a particle set of M particles, fixed when its keys are first
-// computed (bin_keys / load_aos) and kept by the push kernels: box layout for
-// sparse sets on the DMMA path (n % 8 == 0, w <= 8, not deterministic).
-// The crossover density was measured on B200 (sparse sets).
-constexpr double kBoxMaxDensity = 12.0;   // particles per stencil cell
-void choose_layout(Plan &p, int64_t M) {
-    const bool allowed = fast_path_ok(p) && !p.det && p.n % 8 == 0 && p.n >= 16 && !p.wcache_on;
-    const double density = (double)M / (double)p.n3;
-    if (!allowed || p.box_force == 0) p.box = false;
-    else if (p.box_force == 1) p.box = true;
-    else p.box = density < kBoxMaxDensity;
-}
-
 int launch_bin_keys(Plan &p, const pif_soa_t &src, int32_t *key, int32_t *rank, cudaStream_t s) {
-    choose_layout(p, src.count);
     if (src.count == 0) return PIF_OK;
     bin_keys_kernel<<<grid_for(src.count, 256, p.sm_count), 256, 0, s>>>(
-        src.x, src.y, src.z, src.count, p.h, p.w, p.n, p.box ? 1 : 0, key, rank, p.cell_count);
+        src.x, src.y, src.z, src.count, p.h, p.w, p.n, key, rank, p.cell_count);
     return fail_cuda(cudaGetLastError(), "bin_keys_kernel");
 }
 
@@ -2066,10 +1716,9 @@ int debug_phase_cycles(unsigned long long *out) {
 int launch_load_aos(Plan &p, const double *x, const double *v, int64_t id0, pif_soa_t &dst,
                     int32_t *key, int32_t *rank, cudaStream_t s) {
     p.wcache_valid = false;
-    choose_layout(p, dst.count);
     if (dst.count == 0) return PIF_OK;
     load_aos_kernel<<<grid_for(dst.count, 256, p.sm_count), 256, 0, s>>>(
-        x, v, id0, dst.count, dst, p.L, p.h, p.w, p.n, p.box ? 1 : 0, key, rank, p.cell_count);
+        x, v, id0, dst.count, dst, p.L, p.h, p.w, p.n, key, rank, p.cell_count);
     return fail_cuda(cudaGetLastError(), "load_aos_kernel");
 }
 
@@ -2148,34 +1797,7 @@ int launch_spread(Plan &p, const pif_soa_t &P, const int32_t *perm, const double
     if (e != cudaSuccess) return fail_cuda(e, "zero grid");
     if (P.count == 0) return PIF_OK;
     p.wcache_valid = false;
-    if (p.box) {
-        e = cudaMemsetAsync(p.work, 0, sizeof(unsigned int), s);
-        if (e != cudaSuccess) return fail_cuda(e, "zero work counter");
-        const int threads = kBoxWarps * 32;
-        const size_t dyn = kBoxSpreadDyn;
-#define PIF_BOX_SPREAD_CASE(W)                                                               \
-    case W: {                                                                                \
-        auto k = spread_box_kernel<W>;                                                      \
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kBoxSpreadDyn); \
-        int blocks = persistent_blocks(k, threads, dyn, p.sm_count);                         \
-        k<<<blocks, threads, dyn, s>>>(P.x, P.y, P.z, P.id, perm, strengths, q, p.cell_start, \
-                                       p.grid, p.n, p.h, p.beta, poly, p.work);              \
-        break;                                                                               \
-    }
-        switch (p.w) {
-            PIF_BOX_SPREAD_CASE(2)
-            PIF_BOX_SPREAD_CASE(3)
-            PIF_BOX_SPREAD_CASE(4)
-            PIF_BOX_SPREAD_CASE(5)
-            PIF_BOX_SPREAD_CASE(6)
-            PIF_BOX_SPREAD_CASE(7)
-            PIF_BOX_SPREAD_CASE(8)
-            default:
-                set_error("unsupported window width");
-                return PIF_ERR_VALUE;
-        }
-#undef PIF_BOX_SPREAD_CASE
-    } else if (fast_path_ok(p)) {
+    if (fast_path_ok(p)) {
         const int nseg = (p.n + p.seg - 1) / p.seg;
         const int *nitems = p.seg_off + p.n_segs;
         e = cudaMemsetAsync(p.work, 0, sizeof(unsigned int), s);
@@ -2308,35 +1930,7 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
     const double4 *field = reinterpret_cast<const double4 *>(p.field);
     cudaError_t e;
     int blocks = 1;
-    if (P.count > 0 && p.box) {
-        e = cudaMemsetAsync(p.work, 0, sizeof(unsigned int), s);
-        if (e != cudaSuccess) return fail_cuda(e, "zero work counter");
-        const int threads = kBoxWarps * 32;
-#define PIF_BOX_INTERP_CASE(W)                                                                \
-    case W: {                                                                                 \
-        auto k = push ? interp_box_kernel<W, true> : interp_box_kernel<W, false>;             \
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kBoxGatherDyn);  \
-        blocks = persistent_blocks(k, threads, kBoxGatherDyn, p.sm_count);                    \
-        if (blocks > p.partial_blocks) blocks = p.partial_blocks;                             \
-        k<<<blocks, threads, kBoxGatherDyn, s>>>(P, perm, Q, p.cell_start, field, p.beta, poly, \
-                                                 pp, key, rank, p.cell_count, p.partials,      \
-                                                 E_out, p.work);                              \
-        break;                                                                                \
-    }
-        switch (p.w) {
-            PIF_BOX_INTERP_CASE(2)
-            PIF_BOX_INTERP_CASE(3)
-            PIF_BOX_INTERP_CASE(4)
-            PIF_BOX_INTERP_CASE(5)
-            PIF_BOX_INTERP_CASE(6)
-            PIF_BOX_INTERP_CASE(7)
-            PIF_BOX_INTERP_CASE(8)
-            default:
-                set_error("unsupported window width");
-                return PIF_ERR_VALUE;
-        }
-#undef PIF_BOX_INTERP_CASE
-    } else if (P.count > 0 && fast_path_ok(p)) {
+    if (P.count > 0 && fast_path_ok(p)) {
         const int nseg = (p.n + p.seg - 1) / p.seg;
         const int *nitems = p.seg_off + p.n_segs;
         e = cudaMemsetAsync(p.work, 0, sizeof(unsigned int), s);

@@ -94,10 +94,6 @@ struct Plan {
     // deterministic mode (pif_set_deterministic): stable binning + fixed-order
     // plane reduction instead of REDG, diagnostics from a fixed-order pass
     bool det = false;
-    // sparse sets (box mode, particles.cu key_of): cell keys in 8^3-box order and
-    // the box kernels (one CTA per box, field tile / charge tile in shared memory)
-    bool box = false;
-    int box_force = -1;            // env PIF_BOX: -1 auto, 0 never, 1 always (when allowed)
     double *dbuf = nullptr;        // per-item plane slices of the spread
     int64_t dbuf_cap = 0;
     int32_t *det_keys = nullptr, *det_iota = nullptr;
