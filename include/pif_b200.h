@@ -208,6 +208,12 @@ int pif_set_weight_cache(pif_plan_t plan, int enable);
  * around the pushes that should mirror. */
 int pif_load_aos(pif_plan_t plan, const double *x, const double *v, int64_t id0, pif_soa_t *dst,
                  int32_t *key, int32_t *rank, void *stream);
+/* pif_load_aos with v == NULL loads positions (and keys) only, so binning and
+ * the deposit can start while the velocities are still on the way;
+ * pif_load_aos_velocities then fills dst's velocities from the (M,3) rows
+ * (same set, before any push).  rank may be NULL (pif_bin_perm with NULL
+ * rank assigns the in-cell slots). */
+int pif_load_aos_velocities(pif_plan_t plan, const double *v, pif_soa_t *dst, void *stream);
 int pif_set_id_order_output(pif_plan_t plan, double *x_out, double *v_out, int64_t id0);
 /* Diagnostic sums of a particle set (Recorder.record, strategies.py:96-106). */
 int pif_particle_diag(pif_plan_t plan, const pif_soa_t *p, int e_kind, double *diag,

@@ -76,6 +76,7 @@ SIGNATURES = {
     "pif_probe_fp64": ([_P, _I, _I, _I, _P, _D3], _I),
     "pif_debug_phase_cycles": ([_P], _I),
     "pif_load_aos": ([_P, _P, _P, _I64, _SOA, _P, _P, _P], _I),
+    "pif_load_aos_velocities": ([_P, _P, _SOA, _P], _I),
     "pif_set_id_order_output": ([_P, _P, _P, _I64], _I),
     "pif_set_weight_cache": ([_P, _I], _I),
     "pif_type1_complex_sorted": ([_P, _SOA, _P, _P, _P, _P], _I),

@@ -564,8 +564,15 @@ int pif_load_aos(pif_plan_t plan, const double *x, const double *v, int64_t id0,
                  int32_t *key, int32_t *rank, void *stream) {
     PLAN_CHECK();
     if (!pif::soa_ok(dst, true)) return pif::bad("invalid destination view");
-    if (dst->count > 0 && (!x || !v || !key || !rank)) return pif::bad("missing input / key / rank");
+    if (dst->count > 0 && (!x || !key)) return pif::bad("missing input / key");
     return pif::launch_load_aos(p, x, v, id0, *dst, key, rank, s);
+}
+
+int pif_load_aos_velocities(pif_plan_t plan, const double *v, pif_soa_t *dst, void *stream) {
+    PLAN_CHECK();
+    if (!pif::soa_ok(dst, true)) return pif::bad("invalid destination view");
+    if (dst->count > 0 && !v) return pif::bad("missing velocities");
+    return pif::launch_load_velocities(p, v, *dst, s);
 }
 
 int pif_particle_diag(pif_plan_t plan, const pif_soa_t *ps, int e_kind, double *diag,

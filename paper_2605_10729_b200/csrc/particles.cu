@@ -118,13 +118,27 @@ __global__ void load_aos_kernel(const double *__restrict__ xa, const double *__r
         dst.x[i] = x;
         dst.y[i] = y;
         dst.z[i] = z;
-        dst.vx[i] = va[3 * i];
-        dst.vy[i] = va[3 * i + 1];
-        dst.vz[i] = va[3 * i + 2];
+        if (va) {
+            dst.vx[i] = va[3 * i];
+            dst.vy[i] = va[3 * i + 1];
+            dst.vz[i] = va[3 * i + 2];
+        }
         dst.id[i] = id0 + i;
         const int k = cell_key(x, y, z, h, rh, w, n);
         key[i] = k;
-        rank[i] = atomicAdd(&count[k], 1);
+        if (rank) rank[i] = atomicAdd(&count[k], 1);
+        else atomicAdd(&count[k], 1);
+    }
+}
+
+// the velocities of a set loaded with load_aos_kernel(va = NULL): AoS rows of
+// ids id0 .. id0+M-1 -> SoA slots i (the load left particle i in slot i)
+__global__ void load_vel_kernel(const double *__restrict__ va, int64_t M, pif_soa_t dst) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        dst.vx[i] = va[3 * i];
+        dst.vy[i] = va[3 * i + 1];
+        dst.vz[i] = va[3 * i + 2];
     }
 }
 
@@ -1711,6 +1725,12 @@ int debug_phase_cycles(unsigned long long *out) {
     set_error("built without PIF_PHASE_TIMING");
     return PIF_ERR_STATE;
 #endif
+}
+
+int launch_load_velocities(Plan &p, const double *v, pif_soa_t &dst, cudaStream_t s) {
+    if (dst.count == 0) return PIF_OK;
+    load_vel_kernel<<<grid_for(dst.count, 256, p.sm_count), 256, 0, s>>>(v, dst.count, dst);
+    return fail_cuda(cudaGetLastError(), "load_vel_kernel");
 }
 
 int launch_load_aos(Plan &p, const double *x, const double *v, int64_t id0, pif_soa_t &dst,

@@ -134,6 +134,7 @@ int launch_type2_complex_sorted(Plan &p, const double *modes, const pif_soa_t &s
                                 double *E_out, cudaStream_t s);
 int launch_load_aos(Plan &p, const double *x, const double *v, int64_t id0, pif_soa_t &dst,
                     int32_t *key, int32_t *rank, cudaStream_t s);
+int launch_load_velocities(Plan &p, const double *v, pif_soa_t &dst, cudaStream_t s);
 int launch_interp(Plan &p, const pif_soa_t &src, const int32_t *perm, pif_soa_t &dst, bool push,
                   double half, double dt, const double *tq, const double *sq, int has_b,
                   int e_kind, int32_t *key, int32_t *rank, double *diag, double *E_out,

@@ -189,14 +189,23 @@ class PifEngine:
 
     def load_aos(self, x, v, id0: int):
         """Device (M,3) AoS x, v of ids id0 .. id0+M-1 (host ParticleEnsemble
-        layout) -> SoA store, wrapped, binned: one fused pass + perm."""
+        layout) -> SoA store, wrapped, binned: one fused pass + perm.
+        v=None loads positions only (load_velocities later, before the push)."""
         if self.count:
             cur = self._soa()
-            _native.call("pif_load_aos", self.handle, x.data_ptr(), v.data_ptr(), int(id0),
-                         ctypes.byref(cur), self.parts.key.data_ptr(),
-                         self.parts.rank.data_ptr(), self._stream())
+            _native.call("pif_load_aos", self.handle, x.data_ptr(),
+                         None if v is None else v.data_ptr(), int(id0), ctypes.byref(cur),
+                         self.parts.key.data_ptr(), None, self._stream())
             self.launches += 1
             self._bin()
+
+    def load_velocities(self, v):
+        """The velocities of a set loaded by load_aos(x, None, id0)."""
+        if self.count:
+            cur = self._soa()
+            _native.call("pif_load_aos_velocities", self.handle, v.data_ptr(), ctypes.byref(cur),
+                         self._stream())
+            self.launches += 1
 
     def load_sampled(self, spec, id_range, seed: int | None = None):
         """Generate this rank's slice of the reference ensemble directly into the
@@ -414,11 +423,13 @@ class PifEngine:
         solves, gathers + pushes, scatters back to id order and downloads x, v
         into the same host arrays (energy_out[s] <- the step's field energy).
 
-        Copies run on two side streams.  The download of step s and the upload
-        of step s+1 read and write the same host arrays, so they are pipelined
-        chunk by chunk (each chunk's upload waits for its download): the two
-        PCIe directions overlap instead of running back to back.  Pin xh / vh
-        (torch pin_memory) for asynchronous copies."""
+        Positions travel first: binning, the deposit, the allreduce and the
+        field solve of a step only need x, so they run while v is still being
+        uploaded; v is loaded just before the gather + push.  Between steps the
+        arrays round-trip chunk by chunk on two copy streams (each chunk's
+        upload for step s+1 waits for that chunk's download of step s), x
+        chunks first, so both PCIe directions stay busy.  Pin xh / vh (torch
+        pin_memory) for asynchronous copies."""
         torch = require_cuda()
         M, dev = self.count, self.device
         if tuple(xh.shape) != (M, 3) or tuple(vh.shape) != (M, 3):
@@ -431,16 +442,23 @@ class PifEngine:
         xd, vd = self._stage
         step = max(1, -(-M // max(1, n_chunks)))
         bounds = [(i, min(M, i + step)) for i in range(0, M, step)]
+        ev = lambda: torch.cuda.Event()  # noqa: E731
         up.wait_stream(main)
         with torch.cuda.stream(up):
             xd.copy_(xh, non_blocking=True)
+            x_in = ev()
+            x_in.record(up)
             vd.copy_(vh, non_blocking=True)
+            v_in = ev()
+            v_in.record(up)
         for s in range(steps):
-            main.wait_stream(up)
-            self.load_aos(xd, vd, id0)
+            main.wait_event(x_in)
+            self.load_aos(xd, None, id0)
             self.deposit()
             self.allreduce()
             self.solve_fields()
+            main.wait_event(v_in)
+            self.load_velocities(vd)
             # the push also writes x, v in id order into the staging arrays
             _native.call("pif_set_id_order_output", self.handle, xd.data_ptr(), vd.data_ptr(),
                          int(id0))
@@ -452,15 +470,21 @@ class PifEngine:
                 energy_out[s:s + 1].copy_(self.scalars[0:1], non_blocking=True)
             down.wait_stream(main)
             last = s == steps - 1
-            for i0, i1 in bounds:
-                with torch.cuda.stream(down):
-                    xh[i0:i1].copy_(xd[i0:i1], non_blocking=True)
-                    vh[i0:i1].copy_(vd[i0:i1], non_blocking=True)
+            for src, dst_h, which in ((xd, xh, "x"), (vd, vh, "v")):
+                for i0, i1 in bounds:
+                    with torch.cuda.stream(down):
+                        dst_h[i0:i1].copy_(src[i0:i1], non_blocking=True)
+                    if not last:
+                        up.wait_stream(down)
+                        with torch.cuda.stream(up):
+                            src[i0:i1].copy_(dst_h[i0:i1], non_blocking=True)
                 if not last:
-                    up.wait_stream(down)
-                    with torch.cuda.stream(up):
-                        xd[i0:i1].copy_(xh[i0:i1], non_blocking=True)
-                        vd[i0:i1].copy_(vh[i0:i1], non_blocking=True)
+                    e = ev()
+                    e.record(up)
+                    if which == "x":
+                        x_in = e
+                    else:
+                        v_in = e
         main.wait_stream(down)
         main.wait_stream(up)
         for t in (xd, vd):
