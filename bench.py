@@ -353,6 +353,10 @@ def run_b200(a):
                                   "share one ~37 TF/s pipe on B200",
         "kernel": (f"interp_mma_kernel<{w}, 1>" if w <= 8 else f"interp_ring_kernel<{w}, 1>")
                   + " (fused gather + Boris push)",
+        "weight_cache": bool(eng.weight_cache),
+        "weight_cache_note": "the spread keeps its window weights (192 B/particle) and the next "
+                             "gather, at the same positions, loads them instead of evaluating "
+                             "them; algorithmic flops are unchanged (weights are not counted)",
         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
         "traffic": tr,
         "peak_source": "fp64 peak measured live in this run by the DFMA probe (pif_probe_fp64; "

@@ -83,7 +83,8 @@ class PifEngine:
         DMMA kernels are the only deterministic ones)."""
         _native.call("pif_set_deterministic", self.handle, 1 if on else 0)
         self.deterministic = bool(on)
-        if on:
+        if on and self.weight_cache:
+            _native.call("pif_set_weight_cache", self.handle, 0)
             self.weight_cache = False
 
     def configure(self, *, q: float, m: float, externals, dt: float, shape: str = "delta"):
@@ -131,13 +132,19 @@ class PifEngine:
         return eng.configure(q=q, m=m, externals=externals, dt=dt, shape=shape)
 
     def _enable_weight_cache(self) -> bool:
-        """PIF_WEIGHT_CACHE=1: the spread keeps its window weights for the next
-        gather (192 B per particle at w = 8, if HBM has room).  Off by default:
-        on B200 it trades 2 x 25.8 GB of HBM traffic per step at 2^27 particles
-        for the gather's weight evaluation, a net ~2%."""
+        """Spread -> gather weight reuse (pif_set_weight_cache): the spread of
+        step n keeps its 3 x w window weights (192 B per particle at w = 8) and
+        the gather of step n+1, which runs at exactly those positions, loads
+        them instead of evaluating them again.  On B200 at 2^27 particles this
+        trades 2 x 25.8 GB of HBM traffic per step for ~19 clk of FP64 pipe
+        work per particle: gather 19.6 -> 17.6 ms, spread 8.8 -> 9.3 ms, step
+        -4.8% (profiles/round2/scaling/summary_4xB200.txt).  On by default
+        when HBM has room for it (w <= 8, not in deterministic mode);
+        PIF_WEIGHT_CACHE=0 turns it off, =1 asks for it."""
         import os
         torch = require_cuda()
-        want = os.environ.get("PIF_WEIGHT_CACHE", "0").strip() not in ("0", "", "false", "off")
+        env = os.environ.get("PIF_WEIGHT_CACHE", "auto").strip().lower()
+        want = env not in ("0", "false", "off")
         on = False
         if want and self.plan.window.w <= 8:
             free, _ = torch.cuda.mem_get_info(self.device)
