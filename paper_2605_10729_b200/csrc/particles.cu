@@ -837,8 +837,10 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
     __shared__ WarpChunk stage[kGatherWarps];
     __shared__ double4 planes[kGatherWarps][8][8];
     __shared__ double tab[32];
+    __shared__ int seg_cells[kGatherWarps][kMaxSeg + 1];   // this item's cell boundaries
     extern __shared__ double4 dyn_smem[];
     GatherPartials &gpart = reinterpret_cast<GatherPartials *>(dyn_smem)[threadIdx.x >> 5];
+    int *cbt = seg_cells[threadIdx.x >> 5];
     WarpChunk *stage2 = reinterpret_cast<WarpChunk *>(
         reinterpret_cast<GatherPartials *>(dyn_smem) + kGatherWarps);
     if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
@@ -875,11 +877,13 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
         const int ix = col / n, iy = col - ix * n;
         const int k0 = sg * seg, k1 = min(k0 + seg, n);
         const int base = col * n;
-        const int cb = cell_start[base + k0 + min(lane, k1 - k0)];   // seg <= 31
-        const int pbeg = __shfl_sync(kFull, cb, 0) + it.y * kItemParticles;
-        const int pend = min(pbeg + kItemParticles, __shfl_sync(kFull, cb, k1 - k0));
+        __syncwarp();   // the previous item is done with the cell table
+        for (int c = lane; c <= k1 - k0; c += 32) cbt[c] = cell_start[base + k0 + c];
+        __syncwarp();
+        const int pbeg = cbt[0] + it.y * kItemParticles;
+        const int pend = min(pbeg + kItemParticles, cbt[k1 - k0]);
         int kf = k0;   // cell holding the item's first particle
-        while (__shfl_sync(kFull, cb, kf - k0 + 1) <= pbeg) ++kf;
+        while (cbt[kf - k0 + 1] <= pbeg) ++kf;
         const int64_t yrow = (iy + r) % n;
 
         // prefetch the first chunk (positions, velocities, id) before the window;
@@ -904,7 +908,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
             load_plane(g, hh, field, ix, yrow, n, (kf + ((s - kf) & 7)) % n);
         }
         int k = kf;
-        int cell_end = __shfl_sync(kFull, cb, kf - k0 + 1);
+        int cell_end = cbt[kf - k0 + 1];
         prefetch_wait();   // previous item's outstanding prefetch
         if (wc) {          // first chunk's cached weights
             chunk_weights_async<W>(wb ? st1 : st0, wc, wstride, pbeg + lane, lane,
@@ -968,7 +972,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                     ++k;
                     prefetch_plane(pf, field, ix, iy, n, (k + 8) % n, lane);
                     wnewest = false;
-                    cell_end = __shfl_sync(kFull, cb, k - k0 + 1);
+                    cell_end = cbt[k - k0 + 1];
                     continue;
                 }
                 const int m = min(8, min(pos + cnt, cell_end) - gp);
@@ -1670,15 +1674,19 @@ static EsPoly device_poly(const Plan &p) {
     return e;
 }
 
-// Cells per z-segment work item: 8 at the benchmark density (64 particles per
-// stencil cell); sparser sets get longer segments (up to 31, the gather's
-// one-lane-per-cell start table) so an item still holds ~seg_target particles
-// and the per-item window / first-chunk loads stay amortised.
+// Cells per z-segment work item: 16 at the benchmark density (64 particles per
+// stencil cell); sparser sets get longer segments (up to kMaxSeg; 31 for the
+// ring kernels' one-lane-per-cell start table) so an item still holds
+// ~seg_target particles and the per-item window / first-chunk loads stay
+// amortised.
 int segment_cells(const Plan &p, int64_t M) {
     const double per_cell = (double)M / (double)p.n3;
     const double want = (double)p.seg_target / (per_cell > 1.0 ? per_cell : 1.0);
     const int seg = (int)std::ceil(want);
-    return seg < 8 ? 8 : (seg > 31 ? 31 : seg);
+    // the ring gather keeps the cell boundaries one per lane (<= 31 cells); the
+    // DMMA gather keeps them in shared memory (<= kMaxSeg)
+    const int cap = (p.w > kMaxFastW || p.force_ring) ? 31 : kMaxSeg;
+    return seg < 8 ? 8 : (seg > cap ? cap : seg);
 }
 
 int build_items(Plan &p, int64_t M, cudaStream_t s) {

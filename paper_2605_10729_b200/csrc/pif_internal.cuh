@@ -30,6 +30,7 @@ constexpr int kSub = 8;            // particles per warp sub-batch (fast kernels
 constexpr int kWarpsPerBlock = 4;  // fast kernels: one work item per warp
 constexpr int kDiagSlots = 6;
 constexpr int kItemParticles = 1024;   // max particles per work item
+constexpr int kMaxSeg = 127;           // max cells per z-segment work item (DMMA kernels)
 
 // polynomial coefficients for the interior window weights (es_fast.cuh)
 constexpr int kEsDegHost = 14;
