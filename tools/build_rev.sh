@@ -9,6 +9,6 @@ git -C "$root" archive "$rev" paper_2605_10729_b200/csrc include | tar -x -C "$t
 cd "$tmp/paper_2605_10729_b200/csrc"
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
   -Xcompiler -fPIC -shared "$@" -o "$root/paper_2605_10729_b200/lib_$name.so" \
-  $(ls particles.cu fields.cu capi.cu probe.cu sampler.cu 2>/dev/null) -lcufft -Xlinker -rpath=/usr/local/cuda/lib64
+  $(ls particles.cu fields.cu capi.cu probe.cu sampler.cu comm.cu 2>/dev/null) -lcufft -ldl -Xlinker -rpath=/usr/local/cuda/lib64
 rm -rf "$tmp"
 echo "$root/paper_2605_10729_b200/lib_$name.so"
