@@ -823,7 +823,7 @@ constexpr int kGatherFmaMax = PIF_GATHER_FMA_MAX;
 #endif
 constexpr int kGatherWarps = PIF_GATHER_WARPS;   // warps per gather block
 
-template <int W, bool PUSH>
+template <int W, bool PUSH, bool LONGSEG>
 __global__ void __launch_bounds__(kGatherWarps * 32, PIF_INTERP_MINB)
 interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                   const int32_t *__restrict__ cell_start,
@@ -837,10 +837,12 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
     __shared__ WarpChunk stage[kGatherWarps];
     __shared__ double4 planes[kGatherWarps][8][8];
     __shared__ double tab[32];
-    __shared__ int seg_cells[kGatherWarps][kMaxSeg + 1];   // this item's cell boundaries
+    // this item's cell boundaries: one per lane in a register (segments of
+    // <= 31 cells), or a per-warp shared table (LONGSEG: up to kMaxSeg cells)
+    __shared__ int seg_cells[LONGSEG ? kGatherWarps : 1][LONGSEG ? kMaxSeg + 1 : 1];
     extern __shared__ double4 dyn_smem[];
     GatherPartials &gpart = reinterpret_cast<GatherPartials *>(dyn_smem)[threadIdx.x >> 5];
-    int *cbt = seg_cells[threadIdx.x >> 5];
+    int *cbt = seg_cells[LONGSEG ? (threadIdx.x >> 5) : 0];
     WarpChunk *stage2 = reinterpret_cast<WarpChunk *>(
         reinterpret_cast<GatherPartials *>(dyn_smem) + kGatherWarps);
     if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
@@ -877,13 +879,20 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
         const int ix = col / n, iy = col - ix * n;
         const int k0 = sg * seg, k1 = min(k0 + seg, n);
         const int base = col * n;
-        __syncwarp();   // the previous item is done with the cell table
-        for (int c = lane; c <= k1 - k0; c += 32) cbt[c] = cell_start[base + k0 + c];
-        __syncwarp();
-        const int pbeg = cbt[0] + it.y * kItemParticles;
-        const int pend = min(pbeg + kItemParticles, cbt[k1 - k0]);
+        int cb = 0;
+        if (LONGSEG) {
+            __syncwarp();   // the previous item is done with the cell table
+            for (int c = lane; c <= k1 - k0; c += 32) cbt[c] = cell_start[base + k0 + c];
+            __syncwarp();
+        } else {
+            cb = cell_start[base + k0 + min(lane, k1 - k0)];
+        }
+        // boundary t of the item's cells (warp-uniform t)
+        auto bound = [&](int t) { return LONGSEG ? cbt[t] : __shfl_sync(kFull, cb, t); };
+        const int pbeg = bound(0) + it.y * kItemParticles;
+        const int pend = min(pbeg + kItemParticles, bound(k1 - k0));
         int kf = k0;   // cell holding the item's first particle
-        while (cbt[kf - k0 + 1] <= pbeg) ++kf;
+        while (bound(kf - k0 + 1) <= pbeg) ++kf;
         const int64_t yrow = (iy + r) % n;
 
         // prefetch the first chunk (positions, velocities, id) before the window;
@@ -908,7 +917,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
             load_plane(g, hh, field, ix, yrow, n, (kf + ((s - kf) & 7)) % n);
         }
         int k = kf;
-        int cell_end = cbt[kf - k0 + 1];
+        int cell_end = bound(kf - k0 + 1);
         prefetch_wait();   // previous item's outstanding prefetch
         if (wc) {          // first chunk's cached weights
             chunk_weights_async<W>(wb ? st1 : st0, wc, wstride, pbeg + lane, lane,
@@ -972,7 +981,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                     ++k;
                     prefetch_plane(pf, field, ix, iy, n, (k + 8) % n, lane);
                     wnewest = false;
-                    cell_end = cbt[k - k0 + 1];
+                    cell_end = bound(k - k0 + 1);
                     continue;
                 }
                 const int m = min(8, min(pos + cnt, cell_end) - gp);
@@ -1970,10 +1979,11 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
                                : nullptr;
         const size_t dyn = kGatherDyn + (wc ? kGatherWarps * sizeof(WarpChunk) : 0);
         const int gthreads = kGatherWarps * 32;
+        const bool longseg = p.seg > 31;
 #define PIF_INTERP_CASE(W)                                                                    \
     case W: {                                                                                 \
         if (push) {                                                                           \
-            auto k = interp_mma_kernel<W, true>;                                             \
+            auto k = longseg ? interp_mma_kernel<W, true, true> : interp_mma_kernel<W, true, false>; \
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kGatherDynMax); \
             blocks = persistent_blocks(k, gthreads, dyn, p.sm_count);                         \
             if (blocks > p.partial_blocks) blocks = p.partial_blocks;                         \
@@ -1983,7 +1993,8 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
                                          key, rank, p.cell_count, p.partials, E_out, p.work,   \
                                          p.items, nitems, wc, P.count);                       \
         } else {                                                                              \
-            auto k = interp_mma_kernel<W, false>;                                            \
+            auto k = longseg ? interp_mma_kernel<W, false, true>                              \
+                             : interp_mma_kernel<W, false, false>;                            \
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kGatherDynMax); \
             blocks = persistent_blocks(k, gthreads, dyn, p.sm_count);                         \
             k<<<blocks, gthreads, dyn, s>>>(P, perm, Q, p.cell_start, field, p.seg, nseg,     \

@@ -138,13 +138,18 @@ class PifEngine:
         them instead of evaluating them again.  On B200 at 2^27 particles this
         trades 2 x 25.8 GB of HBM traffic per step for ~19 clk of FP64 pipe
         work per particle: gather 19.6 -> 17.6 ms, spread 8.8 -> 9.3 ms, step
-        -4.8% (profiles/round2/scaling/summary_4xB200.txt).  On by default
-        when HBM has room for it (w <= 8, not in deterministic mode);
-        PIF_WEIGHT_CACHE=0 turns it off, =1 asks for it."""
+        -4.8% (profiles/round2/scaling/summary_4xB200.txt); -2.5% at 8 and
+        -3.4% at 16 particles per stencil cell, +3% at 1.25, where the gather
+        is bound by per-cell work, not weights (profiles/round2/seg_length_ab.txt).
+        On by default from 4 particles per stencil cell when HBM has room
+        (w <= 8, not in deterministic mode); PIF_WEIGHT_CACHE=0 turns it off,
+        =1 asks for it at any density."""
         import os
         torch = require_cuda()
         env = os.environ.get("PIF_WEIGHT_CACHE", "auto").strip().lower()
         want = env not in ("0", "false", "off")
+        if env == "auto":
+            want = self.count >= 4 * self.plan.n_up ** 3
         on = False
         if want and self.plan.window.w <= 8:
             free, _ = torch.cuda.mem_get_info(self.device)
