@@ -120,11 +120,15 @@ def _run_replicated(setup: RunSetup, comm: Comm | None, timers: Timers | None,
         table = eng.run(spec.steps, timers=timers)
         host = table.cpu().numpy()
         loop_seconds = _time.perf_counter() - start
-    guard = float(host[:, 6].max()) if host.size else 0.0
-    if guard > 1e-10:
+    # the guard ran on the device every step (pif.py:128-133); the run is not
+    # stopped mid-graph, so report the first offending step as the reference
+    # would have raised there
+    bad = np.nonzero(host[:, 6] > 1e-10)[0] if host.size else []
+    if len(bad):
         from .pif import FieldSymmetryError
-        raise FieldSymmetryError(f"field modes lost Hermitian symmetry (relative mismatch "
-                                 f"{guard:.3e})")
+        first = int(bad[0])
+        raise FieldSymmetryError(f"field modes lost Hermitian symmetry at step {first} "
+                                 f"(relative mismatch {float(host[first, 6]):.3e})")
     recs = records_from_table(host, steps=spec.steps, dt=spec.dt, q=q, m=m,
                               total_charge=spec.Q_e, diag_every=setup.diag_every)
     initial, records = recs[0], recs[1:]
