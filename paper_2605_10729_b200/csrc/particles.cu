@@ -812,6 +812,9 @@ __device__ unsigned long long g_phase_cycles[8];
 #ifndef PIF_INTERP_MINB
 #define PIF_INTERP_MINB 2
 #endif
+#ifndef PIF_INTERP_MINB_WC
+#define PIF_INTERP_MINB_WC 2
+#endif
 // sub-batches of at most this many particles take the FMA path
 #ifndef PIF_GATHER_FMA_MAX
 #define PIF_GATHER_FMA_MAX 3
@@ -823,8 +826,11 @@ constexpr int kGatherFmaMax = PIF_GATHER_FMA_MAX;
 #endif
 constexpr int kGatherWarps = PIF_GATHER_WARPS;   // warps per gather block
 
-template <int W, bool PUSH, bool LONGSEG>
-__global__ void __launch_bounds__(kGatherWarps * 32, PIF_INTERP_MINB)
+// WC: the window weights come from the spread's cache (pif_set_weight_cache)
+// instead of being evaluated here; a separate instantiation so the polynomial
+// code and its registers are not carried when unused.
+template <int W, bool PUSH, bool LONGSEG, bool WC>
+__global__ void __launch_bounds__(kGatherWarps * 32, WC ? PIF_INTERP_MINB_WC : PIF_INTERP_MINB)
 interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                   const int32_t *__restrict__ cell_start,
                   const double4 *__restrict__ field, int seg, int nseg, double beta,
@@ -851,10 +857,10 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
     WarpChunk &st0 = stage[threadIdx.x >> 5];
     // with the weight cache, chunks alternate between two stages (the next
     // chunk's weights land by cp.async while this one is gathered)
-    WarpChunk &st1 = wc ? stage2[threadIdx.x >> 5] : st0;
+    WarpChunk &st1 = WC ? stage2[threadIdx.x >> 5] : st0;
     double4 (*pf)[8] = planes[threadIdx.x >> 5];
     chunk_zero(st0, lane);
-    if (wc) chunk_zero(st1, lane);
+    if (WC) chunk_zero(st1, lane);
     int wb = 0;            // stage of the current chunk
     bool wnewest = false;  // the newest cp.async group holds weights (not a plane)
     const int n = pp.n;
@@ -919,7 +925,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
         int k = kf;
         int cell_end = bound(kf - k0 + 1);
         prefetch_wait();   // previous item's outstanding prefetch
-        if (wc) {          // first chunk's cached weights
+        if (WC) {          // first chunk's cached weights
             chunk_weights_async<W>(wb ? st1 : st0, wc, wstride, pbeg + lane, lane,
                                    min(kChunk, pend - pbeg));
         }
@@ -945,7 +951,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                 npi = perm ? perm[pos + 2 * kChunk + lane] : pos + 2 * kChunk + lane;
             PHASE_MARK(t0);
             WarpChunk &st = wb ? st1 : st0;
-            if (wc) {
+            if (WC) {
                 if (pos + kChunk < pend) {   // next chunk's weights into the other stage
                     chunk_weights_async<W>(wb ? st0 : st1, wc, wstride, pos + kChunk + lane,
                                            lane, min(kChunk, pend - pos - kChunk));
@@ -1032,7 +1038,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
             ph[3] += 1;
             ph[4] += (unsigned long long)cnt;
 #endif
-            if (wc) wb ^= 1;
+            if (WC) wb ^= 1;
         }
     }
 #ifdef PIF_PHASE_TIMING
@@ -1983,7 +1989,10 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
 #define PIF_INTERP_CASE(W)                                                                    \
     case W: {                                                                                 \
         if (push) {                                                                           \
-            auto k = longseg ? interp_mma_kernel<W, true, true> : interp_mma_kernel<W, true, false>; \
+            auto k = longseg ? (wc ? interp_mma_kernel<W, true, true, true>                   \
+                                   : interp_mma_kernel<W, true, true, false>)                 \
+                             : (wc ? interp_mma_kernel<W, true, false, true>                  \
+                                   : interp_mma_kernel<W, true, false, false>);               \
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kGatherDynMax); \
             blocks = persistent_blocks(k, gthreads, dyn, p.sm_count);                         \
             if (blocks > p.partial_blocks) blocks = p.partial_blocks;                         \
@@ -1993,8 +2002,10 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
                                          key, rank, p.cell_count, p.partials, E_out, p.work,   \
                                          p.items, nitems, wc, P.count);                       \
         } else {                                                                              \
-            auto k = longseg ? interp_mma_kernel<W, false, true>                              \
-                             : interp_mma_kernel<W, false, false>;                            \
+            auto k = longseg ? (wc ? interp_mma_kernel<W, false, true, true>                  \
+                                   : interp_mma_kernel<W, false, true, false>)                \
+                             : (wc ? interp_mma_kernel<W, false, false, true>                 \
+                                   : interp_mma_kernel<W, false, false, false>);              \
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kGatherDynMax); \
             blocks = persistent_blocks(k, gthreads, dyn, p.sm_count);                         \
             k<<<blocks, gthreads, dyn, s>>>(P, perm, Q, p.cell_start, field, p.seg, nseg,     \
