@@ -404,10 +404,14 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
     const double rh = __drcp_rn(h);
     __shared__ WarpChunk stage[kWarpsPerBlock];
     __shared__ double tab[32];
+    // the item's cell boundaries, loaded once per item (a per-cell global load
+    // shares a scoreboard with the chunk prefetch and stalls on it)
+    __shared__ int seg_cells[kWarpsPerBlock][kMaxSeg + 1];
     if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
     __syncthreads();
     const int lane = threadIdx.x & 31;
     WarpChunk &st = stage[threadIdx.x >> 5];
+    int *cbt = seg_cells[threadIdx.x >> 5];
     chunk_zero(st, lane);
     const int r = lane >> 2, c4 = lane & 3;
 
@@ -421,8 +425,11 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
         const int ix = col / n, iy = col - ix * n;
         const int k0 = sg * seg, k1 = min(k0 + seg, n);
         const int base = col * n;
-        const int pbeg = cell_start[base + k0] + it.y * kItemParticles;
-        const int pend = min(pbeg + kItemParticles, cell_start[base + k1]);
+        __syncwarp();   // the previous item is done with the cell table
+        for (int c = lane; c <= k1 - k0; c += 32) cbt[c] = cell_start[base + k0 + c];
+        __syncwarp();
+        const int pbeg = cbt[0] + it.y * kItemParticles;
+        const int pend = min(pbeg + kItemParticles, cbt[k1 - k0]);
         const int64_t yrow = (iy + r) % n;   // this lane's footprint row b = r
         const int64_t drow = DET ? ((int64_t)item * 64 + r) * det.stride : 0;
 
@@ -430,10 +437,8 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
 #pragma unroll
         for (int a = 0; a < 8; ++a) acc[a][0] = acc[a][1] = 0.0;
         int k = k0;
-        int cell_end = cell_start[base + k0 + 1];
-        while (cell_end <= pbeg) cell_end = cell_start[base + (++k) + 1];   // first cell
-        // end of the following cell, loaded one cell ahead (k + 2 <= n: cell_start has n3 + 1)
-        int next_end = cell_start[base + min(k + 2, k1)];
+        int cell_end = cbt[1];
+        while (cell_end <= pbeg) cell_end = cbt[(++k) - k0 + 1];   // first cell
 
         double nx = 0.0, ny = 0.0, nz = 0.0, ns = q;
         if (pbeg + lane < pend) {
@@ -466,8 +471,7 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
                 if (pos + j >= cell_end) {
                     spread_flush_plane<W, DET>(acc, k, c4, ix, yrow, n, grid, det, drow, k0);
                     ++k;
-                    cell_end = next_end;
-                    next_end = cell_start[base + min(k + 2, k1)];
+                    cell_end = cbt[k - k0 + 1];
                     continue;
                 }
                 const int jend = min(cnt, cell_end - pos);   // this cell's part of the chunk
