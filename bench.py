@@ -358,6 +358,7 @@ def run_b200(a):
                              "gather, at the same positions, loads them instead of evaluating "
                              "them; algorithmic flops are unchanged (weights are not counted)",
         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+        "frac_vs_nominal_40tf": achieved / 40.0,
         "traffic": tr,
         "peak_source": "fp64 peak measured live in this run by the DFMA probe (pif_probe_fp64; "
                        "DMMA measured equal, profiles/r01_dmma_probe.txt); MEASURED_PEAKS.json "

@@ -69,7 +69,14 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smsp__inst_executed.sum",
-        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"]
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        # atomics: the spread's REDG.ADD.F64 plane flushes and the push's cell counts
+        "l1tex__t_requests_pipe_lsu_mem_global_op_red.sum",
+        "l1tex__t_sectors_pipe_lsu_mem_global_op_red.sum",
+        "lts__t_requests_srcunit_tex_op_red.sum",
+        "lts__t_sectors_srcunit_tex_op_red.sum",
+        "lts__t_sectors_srcunit_tex_op_red.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__t_requests_pipe_lsu_mem_global_op_atom.sum"]
 
 
 def full(path):
