@@ -9,7 +9,9 @@ reference's own seed-0 ensembles regenerated in HBM:
   of ``spread_mma_kernel`` / ``interp_mma_kernel<8,1>`` do the work);
 * Penning 64^3, 2^25 particles (configs[3]'s per-GPU load on 8 GPUs; heavy
   central cells, split work items);
-* Landau 64^3 / 2^22 with the cloud-in-cell shape (pif.py:71-86).
+* Landau 64^3 / 2^22 with the cloud-in-cell shape (pif.py:71-86);
+* Landau 128^3 at 10 particles per mode (the paper's run density, PAPER.md:471:
+  1.25 particles per stencil cell, long sparse work items).
 
 Checked against the oracle (oracle/pif_oracle.{c,py}, pinned to the
 reference's golden vectors in tests/test_oracle.py) on the same initial
@@ -68,11 +70,12 @@ CASES = [
     ("landau", 64, 1 << 27, "delta"),
     ("penning", 64, 1 << 25, "delta"),
     ("landau", 64, 1 << 22, "cic"),
+    ("landau", 128, 10 * 128 ** 3, "delta"),    # the paper's 10 ppm: 1.25 per stencil cell
 ]
 
 
 @pytest.mark.parametrize("kind,N,M,shape", CASES,
-                         ids=[f"{k}-{N}cubed-2p{M.bit_length() - 1}-{s}" for k, N, M, s in CASES])
+                         ids=[f"{k}-{N}cubed-{M // N ** 3}ppm-{s}" for k, N, M, s in CASES])
 def test_engine_step_matches_oracle_at_benchmark_density(kind, N, M, shape, cuda):
     torch = cuda
     from paper_2605_10729_b200.engine import PifEngine
