@@ -225,17 +225,25 @@ __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double
 // 2-way (row strides 33 and 9 doubles).
 constexpr int kChunk = 32;
 
+// Layouts chosen so the hot shared-memory accesses are bank-conflict free
+// (64-bit words, 16 per half-warp phase): wz is [c][p] with row stride 36
+// (= 4 mod 16): the DMMA loops read (c = slot of lane column, p = row lane)
+// and the weight phase writes (p = lane) without conflicts.
+constexpr int kWzStride = kChunk + 4;
 struct WarpChunk {
     double wx[8][kChunk + 1];   // [a][p]  x weights (spreading: times the strength)
     double wy[kChunk][9];       // [p][b]
-    double wz[kChunk][9];       // [p][c]
+    double wz[8][kWzStride];    // [c][p]
     double E[3][kChunk];        // gathered field (gather+push)
 };
 
 // gather: per-particle partial sums over (a, c) for each y offset b, reduced
-// against wy in the push phase instead of a shuffle tree per sub-batch
+// against wy in the push phase instead of a shuffle tree per sub-batch;
+// [b][p] with row stride 34 (= 2 mod 16): the sub-batch stores (b = 2 c4 + j,
+// p = row lane) and the per-particle reads (p = lane) are conflict free
+constexpr int kDStride = kChunk + 2;
 struct GatherPartials {
-    double D[3][kChunk][9];     // [component][p][b]
+    double D[3][8][kDStride];   // [component][b][p]
 };
 
 __device__ __forceinline__ void chunk_zero(WarpChunk &st, int lane) {
@@ -266,7 +274,7 @@ __device__ __forceinline__ void chunk_weights(WarpChunk &st, const double *tab, 
             for (int a = 0; a < W; ++a) {
                 st.wx[a][lane] = scale ? __dmul_rn(s, wt[0][a]) : wt[0][a];
                 st.wy[lane][a] = wt[1][a];
-                st.wz[lane][a] = wt[2][a];
+                st.wz[a][lane] = wt[2][a];
                 if (wc) {
                     wc[a * wstride + wpos] = wt[0][a];
                     wc[(8 + a) * wstride + wpos] = wt[1][a];
@@ -292,7 +300,7 @@ __device__ __forceinline__ void chunk_weights(WarpChunk &st, const double *tab, 
             es_axis_weights<W>(axis_coord(z, h, rh), beta, P, tab, wt);
 #pragma unroll
             for (int a = 0; a < W; ++a) {
-                st.wz[lane][a] = wt[a];
+                st.wz[a][lane] = wt[a];
                 if (wc) wc[(16 + a) * wstride + wpos] = wt[a];
             }
         }
@@ -312,7 +320,7 @@ __device__ __forceinline__ void chunk_weights_async(WarpChunk &st, const double 
         for (int a = 0; a < W; ++a) {
             const unsigned dx = (unsigned)__cvta_generic_to_shared(&st.wx[a][lane]);
             const unsigned dy = (unsigned)__cvta_generic_to_shared(&st.wy[lane][a]);
-            const unsigned dz = (unsigned)__cvta_generic_to_shared(&st.wz[lane][a]);
+            const unsigned dz = (unsigned)__cvta_generic_to_shared(&st.wz[a][lane]);
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dx),
                          "l"(wc + a * wstride + wpos));
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dy),
@@ -483,7 +491,7 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
                 for (; j + 4 <= jend; j += 4) {
                     const int pj = j + c4;
                     const double wyb = st.wy[pj][r];
-                    const double bz = st.wz[pj][zs];
+                    const double bz = st.wz[zs][pj];
 #pragma unroll
                     for (int a = 0; a < 8; ++a)
                         dmma884(acc[a][0], acc[a][1], st.wx[a][pj] * wyb, bz);
@@ -492,7 +500,7 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
                     const bool ok = c4 < jend - j;
                     const int pj = ok ? j + c4 : j;
                     const double wyb = ok ? st.wy[pj][r] : 0.0;
-                    const double bz = st.wz[pj][zs];
+                    const double bz = st.wz[zs][pj];
 #pragma unroll
                     for (int a = 0; a < 8; ++a)
                         dmma884(acc[a][0], acc[a][1], st.wx[a][pj] * wyb, bz);
@@ -685,8 +693,8 @@ __device__ __forceinline__ void gather_sub_d(WarpChunk &st, GatherPartials &gp,
                                              int r, int c4) {
     const int pb = r < m ? j + r : j;
     const double sc = r < m ? 1.0 : 0.0;
-    const double bz0 = sc * st.wz[pb][(c4 - k) & 7];
-    const double bz1 = sc * st.wz[pb][(c4 + 4 - k) & 7];
+    const double bz0 = sc * st.wz[(c4 - k) & 7][pb];
+    const double bz1 = sc * st.wz[(c4 + 4 - k) & 7][pb];
     double A[8][2];
 #pragma unroll
     for (int a = 0; a < 8; ++a) {
@@ -709,8 +717,8 @@ __device__ __forceinline__ void gather_sub_d(WarpChunk &st, GatherPartials &gp,
     if (r < m) {
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-            gp.D[d][j + r][2 * c4] = Dh[0][d][0] + Dh[1][d][0];
-            gp.D[d][j + r][2 * c4 + 1] = Dh[0][d][1] + Dh[1][d][1];
+            gp.D[d][2 * c4][j + r] = Dh[0][d][0] + Dh[1][d][0];
+            gp.D[d][2 * c4 + 1][j + r] = Dh[0][d][1] + Dh[1][d][1];
         }
     }
 }
@@ -735,7 +743,7 @@ __device__ __forceinline__ void gather_sub_fma(WarpChunk &st, GatherPartials &gp
                 h1[d] = fma(g[a][1][d], xa, h1[d]);
             }
         }
-        const double z0 = st.wz[q][s0], z1 = st.wz[q][s1];
+        const double z0 = st.wz[s0][q], z1 = st.wz[s1][q];
         double e[3];
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
@@ -745,7 +753,7 @@ __device__ __forceinline__ void gather_sub_fma(WarpChunk &st, GatherPartials &gp
         }
         if (c4 == 0) {
 #pragma unroll
-            for (int d = 0; d < 3; ++d) gp.D[d][q][r] = e[d];
+            for (int d = 0; d < 3; ++d) gp.D[d][r][q] = e[d];
         }
     }
 }
@@ -762,7 +770,7 @@ __device__ __forceinline__ void gather_reduce(const WarpChunk &st, const GatherP
         double e[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-            e[q] = fma(wy[2 * q + 1], gp.D[d][p][2 * q + 1], wy[2 * q] * gp.D[d][p][2 * q]);
+            e[q] = fma(wy[2 * q + 1], gp.D[d][2 * q + 1][p], wy[2 * q] * gp.D[d][2 * q][p]);
         E[d] = (e[0] + e[1]) + (e[2] + e[3]);
     }
 }
