@@ -18,6 +18,10 @@ import os
 import statistics
 import sys
 
+# the NUFFT operator sweep times type 1 and type 2 as standalone transforms: no
+# spread -> gather weight reuse (that belongs to the PD step, bench.py)
+os.environ.setdefault("PIF_WEIGHT_CACHE", "0")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
