@@ -895,6 +895,9 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                   const __grid_constant__ CUtensorMap fmap, const int use_tma) {
     const int nitems = *n_items;
     __shared__ WarpChunk stage[kGatherWarps];
+    // footprint planes in flight: a ring of kPlaneDepth TMA buffers per warp
+    // (buffer 0 doubles as the cp.async fallback's single buffer)
+    __shared__ __align__(128) double4 planes[kGatherWarps][kPlaneDepth][8][8];
     __shared__ unsigned long long plane_bar[kGatherWarps][kPlaneDepth];
     __shared__ double tab[32];
     // this item's cell boundaries: one per lane in a register (segments of
@@ -905,12 +908,6 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
     int *cbt = seg_cells[LONGSEG ? (threadIdx.x >> 5) : 0];
     WarpChunk *stage2 = reinterpret_cast<WarpChunk *>(
         reinterpret_cast<GatherPartials *>(dyn_smem) + kGatherWarps);
-    // footprint planes in flight: a ring of kPlaneDepth TMA buffers per warp
-    // (buffer 0 doubles as the cp.async fallback's single buffer), dynamic
-    // shared memory after the stages, 128-byte aligned for the TMA
-    typedef double4 Plane[8][8];
-    Plane(*planes)[kPlaneDepth] = reinterpret_cast<Plane(*)[kPlaneDepth]>(
-        (reinterpret_cast<uintptr_t>(stage2 + (WC ? kGatherWarps : 0)) + 127) & ~uintptr_t(127));
     if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -2043,8 +2040,7 @@ int launch_spread(Plan &p, const pif_soa_t &P, const int32_t *perm, const double
 
 // dynamic shared memory of interp_mma_kernel: the per-warp partial sums (+ the
 // second weight stage when the weight cache is in use)
-constexpr int kGatherPlanes = (int)(kGatherWarps * kPlaneDepth * 64 * sizeof(double4)) + 128;
-constexpr int kGatherDyn = (int)(kGatherWarps * sizeof(GatherPartials)) + kGatherPlanes;
+constexpr int kGatherDyn = (int)(kGatherWarps * sizeof(GatherPartials));
 constexpr int kGatherDynMax = kGatherDyn + (int)(kGatherWarps * sizeof(WarpChunk));
 
 // spread -> gather window-weight cache, [24][M] doubles, grown on demand
