@@ -821,18 +821,16 @@ __device__ __forceinline__ void tma_plane(double4 (*pf)[8], const CUtensorMap *m
         : "memory");
 }
 
-// wait for the current phase of buffer i's mbarrier (bit i of `phases`)
-__device__ __forceinline__ void tma_wait(unsigned long long *bar, unsigned &phases, int i) {
+__device__ __forceinline__ void tma_wait(unsigned long long *bar, unsigned &phase) {
     const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-    const unsigned ph = (phases >> i) & 1u;
     unsigned ok = 0;
     do {
         asm volatile(
             "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;"
             " selp.u32 %0, 1, 0, p; }"
-            : "=r"(ok) : "r"(b), "r"(ph) : "memory");
+            : "=r"(ok) : "r"(b), "r"(phase) : "memory");
     } while (!ok);
-    phases ^= 1u << i;
+    phase ^= 1;
 }
 
 __device__ __forceinline__ void plane_from_smem(double (&g)[8][2][3], int hh, double4 (*pf)[8],
@@ -867,13 +865,6 @@ __device__ unsigned long long g_phase_cycles[8];
 #endif
 constexpr int kGatherFmaMax = PIF_GATHER_FMA_MAX;
 
-// footprint planes in flight per gather warp (TMA ring; > 1 hides the load
-// latency where cells hold few particles)
-#ifndef PIF_PLANE_DEPTH
-#define PIF_PLANE_DEPTH 1
-#endif
-constexpr int kPlaneDepth = PIF_PLANE_DEPTH;
-
 #ifndef PIF_GATHER_WARPS
 #define PIF_GATHER_WARPS 4
 #endif
@@ -895,10 +886,8 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                   const __grid_constant__ CUtensorMap fmap, const int use_tma) {
     const int nitems = *n_items;
     __shared__ WarpChunk stage[kGatherWarps];
-    // footprint planes in flight: a ring of kPlaneDepth TMA buffers per warp
-    // (buffer 0 doubles as the cp.async fallback's single buffer)
-    __shared__ __align__(128) double4 planes[kGatherWarps][kPlaneDepth][8][8];
-    __shared__ unsigned long long plane_bar[kGatherWarps][kPlaneDepth];
+    __shared__ __align__(128) double4 planes[kGatherWarps][8][8];
+    __shared__ unsigned long long plane_bar[kGatherWarps];
     __shared__ double tab[32];
     // this item's cell boundaries: one per lane in a register (segments of
     // <= 31 cells), or a per-warp shared table (LONGSEG: up to kMaxSeg cells)
@@ -915,13 +904,11 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
     // with the weight cache, chunks alternate between two stages (the next
     // chunk's weights land by cp.async while this one is gathered)
     WarpChunk &st1 = WC ? stage2[threadIdx.x >> 5] : st0;
-    double4 (*pf)[8] = planes[threadIdx.x >> 5][0];
-    unsigned long long *pbar = plane_bar[threadIdx.x >> 5];
-    unsigned pphase = 0;     // bit i: phase of buffer i's mbarrier to wait for
-    int phead = 0;           // buffer holding the next plane to consume (k + 8)
-    int pinfl = 0;           // TMA plane loads in flight
-    if (use_tma && lane == 0)
-        for (int i = 0; i < kPlaneDepth; ++i) plane_bar_init(&pbar[i]);
+    double4 (*pf)[8] = planes[threadIdx.x >> 5];
+    unsigned long long *pbar = &plane_bar[threadIdx.x >> 5];
+    unsigned pphase = 0;     // phase of the plane mbarrier to wait for
+    bool ppend = false;      // a TMA plane load is in flight
+    if (use_tma && lane == 0) plane_bar_init(pbar);
     chunk_zero(st0, lane);   // (ends with __syncwarp: the barrier is initialised)
     if (WC) chunk_zero(st1, lane);
     int wb = 0;            // stage of the current chunk
@@ -987,28 +974,20 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
         }
         int k = kf;
         int cell_end = bound(kf - k0 + 1);
-        // previous item's outstanding plane loads
+        // previous item's outstanding plane load
         if (!use_tma) {
             prefetch_wait();
-        } else {
-            for (; pinfl > 0; --pinfl) {
-                tma_wait(&pbar[phead], pphase, phead);
-                phead = phead + 1 == kPlaneDepth ? 0 : phead + 1;
-            }
+        } else if (ppend) {
+            tma_wait(pbar, pphase);
             __syncwarp();
         }
         if (WC) {          // first chunk's cached weights
             chunk_weights_async<W>(wb ? st1 : st0, wc, wstride, pbeg + lane, lane,
                                    min(kChunk, pend - pbeg));
         }
-        if (use_tma) {     // planes kf + 8 .. kf + 7 + kPlaneDepth
-            if (lane == 0)
-                for (int t = 0; t < kPlaneDepth; ++t) {
-                    const int bi = (phead + t) % kPlaneDepth;
-                    tma_plane(planes[threadIdx.x >> 5][bi], &fmap, &pbar[bi], ix, iy,
-                              (kf + 8 + t) % n);
-                }
-            pinfl = kPlaneDepth;
+        if (use_tma) {
+            if (lane == 0) tma_plane(pf, &fmap, pbar, ix, iy, (kf + 8) % n);
+            ppend = true;
         } else {
             prefetch_plane(pf, field, ix, iy, n, (kf + 8) % n, lane);
         }
@@ -1055,9 +1034,8 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                 const int gp = pos + j;
                 if (gp >= cell_end) {   // next cell: plane k leaves slot k&7, plane k+8 enters
                     const int s = k & 7;
-                    double4 (*cur)[8] = use_tma ? planes[threadIdx.x >> 5][phead] : pf;
                     if (use_tma) {
-                        tma_wait(&pbar[phead], pphase, phead);
+                        tma_wait(pbar, pphase);
                     } else if (wnewest) {   // the plane group is older than the weights group
                         asm volatile("cp.async.wait_group 1;" ::: "memory");
                         __syncwarp();
@@ -1065,16 +1043,13 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                         prefetch_wait();
                     }
                     if (c4 == (s & 3)) {
-                        if (s >> 2) plane_from_smem(g, 1, cur, r);
-                        else plane_from_smem(g, 0, cur, r);
+                        if (s >> 2) plane_from_smem(g, 1, pf, r);
+                        else plane_from_smem(g, 0, pf, r);
                     }
                     __syncwarp();
                     ++k;
-                    if (use_tma) {   // the freed buffer takes plane k + 7 + kPlaneDepth
-                        if (lane == 0)
-                            tma_plane(cur, &fmap, &pbar[phead], ix, iy,
-                                      (k + 7 + kPlaneDepth) % n);
-                        phead = phead + 1 == kPlaneDepth ? 0 : phead + 1;
+                    if (use_tma) {
+                        if (lane == 0) tma_plane(pf, &fmap, pbar, ix, iy, (k + 8) % n);
                     } else {
                         prefetch_plane(pf, field, ix, iy, n, (k + 8) % n, lane);
                         wnewest = false;
@@ -1137,14 +1112,8 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
     if (lane == 0)
         for (int i = 0; i < 5; ++i) atomicAdd(&g_phase_cycles[i], ph[i]);
 #endif
-    if (!use_tma) {
-        prefetch_wait();
-    } else {   // no TMA write may outlive the block
-        for (; pinfl > 0; --pinfl) {
-            tma_wait(&pbar[phead], pphase, phead);
-            phead = phead + 1 == kPlaneDepth ? 0 : phead + 1;
-        }
-    }
+    if (!use_tma) prefetch_wait();
+    else if (ppend) tma_wait(pbar, pphase);   // no TMA write may outlive the block
     if (PUSH && rank_idx >= 0) rank[rank_idx] = rank_val;
     if (PUSH) block_diag_store(dg, partials);
 }
