@@ -796,43 +796,6 @@ __device__ __forceinline__ void prefetch_wait() {
     __syncwarp();
 }
 
-// The same plane by TMA: one elected lane issues a 4 x 1 x 8 x 8 box load of the
-// halo'd field grid (p.fmap: comps, z, y, x) into pf, completing on the warp's
-// mbarrier; no per-lane address arithmetic, no wrap (the halo covers it).
-__device__ __forceinline__ void plane_bar_init(unsigned long long *bar) {
-    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
-__device__ __forceinline__ void tma_plane(double4 (*pf)[8], const CUtensorMap *map,
-                                          unsigned long long *bar, int ix, int iy, int z) {
-    const unsigned dst = (unsigned)__cvta_generic_to_shared(&pf[0][0]);
-    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-    // the warp's generic-proxy reads of pf (synced before the call) come before
-    // this async-proxy write
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(2048)
-                 : "memory");
-    asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
-        "l"(reinterpret_cast<unsigned long long>(map)), "r"(0), "r"(z), "r"(iy), "r"(ix), "r"(b)
-        : "memory");
-}
-
-__device__ __forceinline__ void tma_wait(unsigned long long *bar, unsigned &phase) {
-    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-    unsigned ok = 0;
-    do {
-        asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;"
-            " selp.u32 %0, 1, 0, p; }"
-            : "=r"(ok) : "r"(b), "r"(phase) : "memory");
-    } while (!ok);
-    phase ^= 1;
-}
-
 __device__ __forceinline__ void plane_from_smem(double (&g)[8][2][3], int hh, double4 (*pf)[8],
                                                 int r) {
 #pragma unroll
@@ -882,12 +845,10 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                   int32_t *__restrict__ rank, int32_t *__restrict__ count,
                   double *__restrict__ partials, double *__restrict__ E_out, unsigned int *work,
                   const int2 *__restrict__ items, const int *__restrict__ n_items,
-                  const double *__restrict__ wc, int64_t wstride,
-                  const __grid_constant__ CUtensorMap fmap, const int use_tma) {
+                  const double *__restrict__ wc, int64_t wstride) {
     const int nitems = *n_items;
     __shared__ WarpChunk stage[kGatherWarps];
-    __shared__ __align__(128) double4 planes[kGatherWarps][8][8];
-    __shared__ unsigned long long plane_bar[kGatherWarps];
+    __shared__ double4 planes[kGatherWarps][8][8];
     __shared__ double tab[32];
     // this item's cell boundaries: one per lane in a register (segments of
     // <= 31 cells), or a per-warp shared table (LONGSEG: up to kMaxSeg cells)
@@ -905,11 +866,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
     // chunk's weights land by cp.async while this one is gathered)
     WarpChunk &st1 = WC ? stage2[threadIdx.x >> 5] : st0;
     double4 (*pf)[8] = planes[threadIdx.x >> 5];
-    unsigned long long *pbar = &plane_bar[threadIdx.x >> 5];
-    unsigned pphase = 0;     // phase of the plane mbarrier to wait for
-    bool ppend = false;      // a TMA plane load is in flight
-    if (use_tma && lane == 0) plane_bar_init(pbar);
-    chunk_zero(st0, lane);   // (ends with __syncwarp: the barrier is initialised)
+    chunk_zero(st0, lane);
     if (WC) chunk_zero(st1, lane);
     int wb = 0;            // stage of the current chunk
     bool wnewest = false;  // the newest cp.async group holds weights (not a plane)
@@ -974,23 +931,12 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
         }
         int k = kf;
         int cell_end = bound(kf - k0 + 1);
-        // previous item's outstanding plane load
-        if (!use_tma) {
-            prefetch_wait();
-        } else if (ppend) {
-            tma_wait(pbar, pphase);
-            __syncwarp();
-        }
+        prefetch_wait();   // previous item's outstanding prefetch
         if (WC) {          // first chunk's cached weights
             chunk_weights_async<W>(wb ? st1 : st0, wc, wstride, pbeg + lane, lane,
                                    min(kChunk, pend - pbeg));
         }
-        if (use_tma) {
-            if (lane == 0) tma_plane(pf, &fmap, pbar, ix, iy, (kf + 8) % n);
-            ppend = true;
-        } else {
-            prefetch_plane(pf, field, ix, iy, n, (kf + 8) % n, lane);
-        }
+        prefetch_plane(pf, field, ix, iy, n, (kf + 8) % n, lane);
         wnewest = false;
 
         for (int pos = pbeg; pos < pend; pos += kChunk) {
@@ -1034,9 +980,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                 const int gp = pos + j;
                 if (gp >= cell_end) {   // next cell: plane k leaves slot k&7, plane k+8 enters
                     const int s = k & 7;
-                    if (use_tma) {
-                        tma_wait(pbar, pphase);
-                    } else if (wnewest) {   // the plane group is older than the weights group
+                    if (wnewest) {   // the plane group is older than the weights group
                         asm volatile("cp.async.wait_group 1;" ::: "memory");
                         __syncwarp();
                     } else {
@@ -1048,12 +992,8 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                     }
                     __syncwarp();
                     ++k;
-                    if (use_tma) {
-                        if (lane == 0) tma_plane(pf, &fmap, pbar, ix, iy, (k + 8) % n);
-                    } else {
-                        prefetch_plane(pf, field, ix, iy, n, (k + 8) % n, lane);
-                        wnewest = false;
-                    }
+                    prefetch_plane(pf, field, ix, iy, n, (k + 8) % n, lane);
+                    wnewest = false;
                     cell_end = bound(k - k0 + 1);
                     continue;
                 }
@@ -1112,8 +1052,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
     if (lane == 0)
         for (int i = 0; i < 5; ++i) atomicAdd(&g_phase_cycles[i], ph[i]);
 #endif
-    if (!use_tma) prefetch_wait();
-    else if (ppend) tma_wait(pbar, pphase);   // no TMA write may outlive the block
+    prefetch_wait();
     if (PUSH && rank_idx >= 0) rank[rank_idx] = rank_val;
     if (PUSH) block_diag_store(dg, partials);
 }
@@ -2068,8 +2007,7 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
                                                   p.beta,                                     \
                                          poly, pp,                                            \
                                          key, rank, p.cell_count, p.partials, E_out, p.work,   \
-                                         p.items, nitems, wc, P.count, p.fmap,                \
-                                         p.tma ? 1 : 0);                                      \
+                                         p.items, nitems, wc, P.count);                       \
         } else {                                                                              \
             auto k = longseg ? (wc ? interp_mma_kernel<W, false, true, true>                  \
                                    : interp_mma_kernel<W, false, true, false>)                \
@@ -2081,8 +2019,7 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
                                                   p.beta,                                     \
                                          poly, pp,                                            \
                                          key, rank, p.cell_count, p.partials, E_out, p.work,   \
-                                         p.items, nitems, wc, P.count, p.fmap,                \
-                                         p.tma ? 1 : 0);                                      \
+                                         p.items, nitems, wc, P.count);                       \
         }                                                                                     \
         break;                                                                                \
     }
