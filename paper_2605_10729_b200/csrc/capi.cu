@@ -221,8 +221,7 @@ int pif_plan_create(const pif_plan_desc_t *d, int device, pif_plan_t *out) {
     TRY(pif::dalloc(p, &p.shape_tab, 2 * p.N));
     TRY(pif::dalloc(p, &p.grid, p.n3));
     TRY(pif::dalloc(p, &p.spec, 3 * p.nhalf));
-    p.nfield = (int64_t)(p.n + pif::kFieldHalo) * (p.n + pif::kFieldHalo) * p.n;
-    TRY(pif::dalloc(p, &p.field, 4 * p.nfield));
+    TRY(pif::dalloc(p, &p.field, 4 * p.n3));
     TRY(pif::dalloc(p, &p.emodes, 3 * N3));
     TRY(pif::dalloc(p, &p.cell_count, p.n3 + 1));
     TRY(pif::dalloc(p, &p.cell_start, p.n3 + 1));
@@ -246,7 +245,7 @@ int pif_plan_create(const pif_plan_desc_t *d, int device, pif_plan_t *out) {
                            cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMemset(p.cell_count, 0, sizeof(int32_t) * (p.n3 + 1));
         if (e == cudaSuccess) e = cudaMemset(p.seg_off, 0, sizeof(int) * (p.n_segs + 1));
-        if (e == cudaSuccess) e = cudaMemset(p.field, 0, sizeof(double) * 4 * p.nfield);
+        if (e == cudaSuccess) e = cudaMemset(p.field, 0, sizeof(double) * 4 * p.n3);
         if (e != cudaSuccess) {
             rc = pif::fail_cuda(e, "plan tables");
             goto fail;
@@ -269,16 +268,14 @@ int pif_plan_create(const pif_plan_desc_t *d, int device, pif_plan_t *out) {
         }
         int dims[3] = {p.n, p.n, p.n};
         int inembed[3] = {p.n, p.n, p.n / 2 + 1};
-        // Z2D straight into the interleaved (Ex,Ey,Ez,0) grid: ostride 4, odist 1,
-        // rows of the halo'd layout (fidx)
-        int onembed[3] = {p.n + pif::kFieldHalo, p.n + pif::kFieldHalo, p.n};
+        int onembed[3] = {p.n, p.n, p.n};
+        // Z2D straight into the interleaved (Ex,Ey,Ez,0) grid: ostride 4, odist 1
         r = cufftPlanMany(&p.z2d3, 3, dims, inembed, 1, (int)p.nhalf, onembed, 4, 1, CUFFT_Z2D, 3);
         if (r == CUFFT_SUCCESS) {
             p.z2d_strided = true;
         } else {
             p.z2d3 = 0;
-            int plain[3] = {p.n, p.n, p.n};
-            r = cufftPlanMany(&p.z2d3, 3, dims, inembed, 1, (int)p.nhalf, plain, 1, (int)p.n3,
+            r = cufftPlanMany(&p.z2d3, 3, dims, inembed, 1, (int)p.nhalf, onembed, 1, (int)p.n3,
                               CUFFT_Z2D, 3);
             if (r != CUFFT_SUCCESS) {
                 rc = pif::fail_cufft(r, "cufftPlanMany(Z2D)");
@@ -288,7 +285,6 @@ int pif_plan_create(const pif_plan_desc_t *d, int device, pif_plan_t *out) {
         }
     }
 #undef TRY
-    pif::encode_field_tma(p);
     *out = h;
     return PIF_OK;
 fail:

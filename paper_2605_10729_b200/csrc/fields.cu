@@ -5,8 +5,6 @@
 // field components (nufft.py:148-156) written as Hermitian-symmetrised half
 // spectra so one batched Z2D reproduces Re(ifftn(pad)) (nufft.py:184-185).
 // All of this is O(N^3) or O(n^3) per step; the particle kernels dominate.
-#include <cstdlib>
-
 #include "pif_internal.cuh"
 
 namespace pif {
@@ -204,33 +202,10 @@ __global__ void pad_half_kernel(const double2 *__restrict__ ex, const double2 *_
 }
 
 __global__ void interleave_kernel(const double *__restrict__ f3, double4 *__restrict__ out,
-                                  int n) {
-    const int64_t n3 = (int64_t)n * n * n;
+                                  int64_t n3) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n3;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t z = i % n, y = (i / n) % n, x = i / ((int64_t)n * n);
-        out[fidx(x, y, z, n)] = make_double4(f3[i], f3[n3 + i], f3[2 * n3 + i], 0.0);
-    }
-}
-
-// Periodic halo of the field grid: rows y = n .. n+6 of x < n, then rows
-// x = n .. n+6 (all y, so the corner comes from the already filled rows).
-__global__ void halo_y_kernel(double4 *__restrict__ f, int n) {
-    const int64_t cnt = (int64_t)n * kFieldHalo * n;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t z = i % n, hy = (i / n) % kFieldHalo, x = i / ((int64_t)n * kFieldHalo);
-        f[fidx(x, n + hy, z, n)] = f[fidx(x, hy % n, z, n)];
-    }
-}
-__global__ void halo_x_kernel(double4 *__restrict__ f, int n) {
-    const int ny = n + kFieldHalo;
-    const int64_t cnt = (int64_t)kFieldHalo * ny * n;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t z = i % n, y = (i / n) % ny, hx = i / ((int64_t)n * ny);
-        f[fidx(n + hx, y, z, n)] = f[fidx(hx % n, y, z, n)];
-    }
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = make_double4(f3[i], f3[n3 + i], f3[2 * n3 + i], 0.0);
 }
 
 // complex API helpers: full-spectrum truncate / pad
@@ -275,49 +250,6 @@ int blocks_for(int64_t work, int threads, int sm_count, int cap_per_sm = 16) {
     return (int)(b < 1 ? 1 : b);
 }
 
-}  // namespace
-
-// TMA descriptor of the interleaved field grid: 4 doubles x n (z) x (n+7) (y)
-// x (n+7) (x), boxes of 4 x 1 x 8 x 8 = one 2 KB footprint plane.  The driver's
-// encoder is looked up at run time (no libcuda link); without it the gather
-// keeps its cp.async plane loads.
-void encode_field_tma(Plan &p) {
-    p.tma = false;
-    void *fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
-            cudaSuccess ||
-        q != cudaDriverEntryPointSuccess || !fn) {
-        cudaGetLastError();
-        return;
-    }
-    using Encode = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
-                                const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
-                                const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-    const cuuint64_t ny = (cuuint64_t)(p.n + kFieldHalo);
-    const cuuint64_t dims[4] = {4, (cuuint64_t)p.n, ny, ny};
-    const cuuint64_t strides[3] = {32, 32 * (cuuint64_t)p.n, 32 * (cuuint64_t)p.n * ny};
-    const cuuint32_t box[4] = {4, 1, 8, 8};
-    const cuuint32_t estr[4] = {1, 1, 1, 1};
-    const CUresult r = reinterpret_cast<Encode>(fn)(
-        &p.fmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, p.field, dims, strides, box, estr,
-        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    p.tma = (r == CUDA_SUCCESS) && std::getenv("PIF_NO_TMA") == nullptr;
-}
-
-namespace {
-
-int fill_field_halo(Plan &p, cudaStream_t s) {
-    double4 *f = reinterpret_cast<double4 *>(p.field);
-    const int64_t cnt = (int64_t)p.n * kFieldHalo * p.n;
-    halo_y_kernel<<<blocks_for(cnt, 256, p.sm_count), 256, 0, s>>>(f, p.n);
-    halo_x_kernel<<<blocks_for(cnt + (int64_t)kFieldHalo * kFieldHalo * p.n, 256, p.sm_count), 256,
-                    0, s>>>(f, p.n);
-    return fail_cuda(cudaGetLastError(), "field halo");
-}
-
 int exec_z2d_fields(Plan &p, cudaStream_t s) {
     cufftResult r = cufftSetStream(p.z2d3, s);
     if (r != CUFFT_SUCCESS) return fail_cufft(r, "cufftSetStream(z2d)");
@@ -329,13 +261,9 @@ int exec_z2d_fields(Plan &p, cudaStream_t s) {
         r = cufftExecZ2D(p.z2d3, reinterpret_cast<cufftDoubleComplex *>(p.spec), p.field3);
         if (r != CUFFT_SUCCESS) return fail_cufft(r, "cufftExecZ2D");
         interleave_kernel<<<blocks_for(p.n3, 256, p.sm_count), 256, 0, s>>>(
-            p.field3, reinterpret_cast<double4 *>(p.field), p.n);
+            p.field3, reinterpret_cast<double4 *>(p.field), p.n3);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return fail_cuda(e, "interleave_kernel");
-    }
-    {
-        const int rc = fill_field_halo(p, s);
-        if (rc != PIF_OK) return rc;
     }
     fft_mark(p, true, true, s);
     p.field_valid = true;
@@ -461,13 +389,11 @@ __global__ void complex_part_kernel(const double *__restrict__ grid, double2 *__
 }
 
 __global__ void pack_complex_field_kernel(const double2 *__restrict__ cgrid,
-                                          double4 *__restrict__ field, int n) {
-    const int64_t n3 = (int64_t)n * n * n;
+                                          double4 *__restrict__ field, int64_t n3) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n3;
          i += (int64_t)gridDim.x * blockDim.x) {
         const double2 c = cgrid[i];
-        const int64_t z = i % n, y = (i / n) % n, x = i / ((int64_t)n * n);
-        field[fidx(x, y, z, n)] = make_double4(c.x, c.y, 0.0, 0.0);
+        field[i] = make_double4(c.x, c.y, 0.0, 0.0);
     }
 }
 
@@ -519,11 +445,9 @@ int launch_type2_complex_sorted(Plan &p, const double *modes, const pif_soa_t &s
                          reinterpret_cast<cufftDoubleComplex *>(p.cgrid), CUFFT_INVERSE);
     if (r != CUFFT_SUCCESS) return fail_cufft(r, "cufftExecZ2Z inverse");
     pack_complex_field_kernel<<<blocks_for(p.n3, 256, p.sm_count), 256, 0, s>>>(
-        p.cgrid, reinterpret_cast<double4 *>(p.field), p.n);
+        p.cgrid, reinterpret_cast<double4 *>(p.field), p.n3);
     e = cudaGetLastError();
     if (e != cudaSuccess) return fail_cuda(e, "pack_complex_field_kernel");
-    rc = fill_field_halo(p, s);
-    if (rc != PIF_OK) return rc;
     p.field_valid = true;
     pif_soa_t v = sorted;
     return launch_interp(p, v, nullptr, v, false, 0.0, 1.0, nullptr, nullptr, 0, PIF_EXT_NONE,

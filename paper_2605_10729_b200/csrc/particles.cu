@@ -669,9 +669,10 @@ __device__ __forceinline__ void load_plane(double (&g)[8][2][3], int hh, const d
                                            int ix, int64_t yrow, int n, int64_t z) {
 #pragma unroll
     for (int a = 0; a < 8; ++a) {
-        const int xa = ix + a;   // <= n + 6: the halo rows of the field grid
-        PIF_CHECK(xa >= 0 && xa < n + kFieldHalo && yrow >= 0 && yrow < n && z >= 0 && z < n);
-        const double4 f = field[fidx(xa, yrow, z, n)];
+        int xa = ix + a;
+        xa = xa >= n ? xa - n : xa;
+        PIF_CHECK(xa >= 0 && xa < n && yrow >= 0 && yrow < n && z >= 0 && z < n);
+        const double4 f = field[((int64_t)xa * n + yrow) * n + z];
         g[a][hh][0] = f.x;
         g[a][hh][1] = f.y;
         g[a][hh][2] = f.z;
@@ -782,7 +783,11 @@ __device__ __forceinline__ void prefetch_plane(double4 (*pf)[8], const double4 *
     for (int t = 0; t < 4; ++t) {
         const int q = lane + 32 * t;              // 16-byte chunk: (a, b, half)
         const int a = q >> 4, b = (q >> 1) & 7, hf = q & 1;
-        const char *src = reinterpret_cast<const char *>(field + fidx(ix + a, iy + b, z, n)) +
+        int xa = ix + a;
+        xa = xa >= n ? xa - n : xa;
+        int yb = iy + b;
+        yb = yb >= n ? yb - n : yb;
+        const char *src = reinterpret_cast<const char *>(field + ((int64_t)xa * n + yb) * n + z) +
                           16 * hf;
         const unsigned dst =
             (unsigned)__cvta_generic_to_shared(reinterpret_cast<char *>(&pf[a][b]) + 16 * hf);
@@ -1253,7 +1258,7 @@ __device__ __forceinline__ void ring_load_plane(double (&g)[(W * W + 31) / 32][W
                 if (qq < W * W) {
                     const int a = qq / W, b = qq - (qq / W) * W;
                     const double *f = reinterpret_cast<const double *>(
-                        field + fidx((ix + a) % n, (iy + b) % n, z, n));
+                        field + ((int64_t)((ix + a) % n) * n + (iy + b) % n) * n + z);
                     v = __ldg(f + comp);
                 }
                 g[t][s] = v;
@@ -1446,7 +1451,7 @@ __global__ void interp_generic_kernel(pif_soa_t P, const int32_t *__restrict__ p
         for (int a = 0; a < w; ++a)
             for (int b = 0; b < w; ++b) {
                 const double wab = __dmul_rn(wx[a], wy[b]);
-                const double4 *row = field + fidx(ixs[a], iys[b], 0, n);
+                const double4 *row = field + ((int64_t)ixs[a] * n + iys[b]) * n;
                 for (int c = 0; c < w; ++c) {
                     const double4 g = row[izs[c]];
                     l0[c] = __dadd_rn(l0[c], __dmul_rn(g.x, wab));

@@ -1,7 +1,6 @@
 // Internal declarations shared by the CUDA translation units of libpifb200.
 #pragma once
 
-#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cufft.h>
 #include <stdint.h>
@@ -32,13 +31,6 @@ constexpr int kWarpsPerBlock = 4;  // fast kernels: one work item per warp
 constexpr int kDiagSlots = 6;
 constexpr int kItemParticles = 1024;   // max particles per work item
 constexpr int kMaxSeg = 127;           // max cells per z-segment work item (DMMA kernels)
-// The interleaved field grid carries kFieldHalo periodic copies past x = n-1
-// and y = n-1, so an 8 x 8 footprint plane of any column is one in-bounds
-// box (one TMA load, no wrap arithmetic): point (x, y, z) at fidx(x, y, z).
-constexpr int kFieldHalo = 7;
-__host__ __device__ inline int64_t fidx(int64_t x, int64_t y, int64_t z, int n) {
-    return (x * (n + kFieldHalo) + y) * n + z;
-}
 
 // polynomial coefficients for the interior window weights (es_fast.cuh)
 constexpr int kEsDegHost = 14;
@@ -52,9 +44,6 @@ struct Plan {
     int N = 0, n = 0, w = 0, device = 0;
     double L = 0, eps = 0, beta = 0, h = 0, inv_L3 = 0, half_L3 = 0;
     int64_t n3 = 0, nhalf = 0;     // n^3, n*n*(n/2+1)
-    int64_t nfield = 0;            // (n + kFieldHalo)^2 * n points of the field grid
-    CUtensorMap fmap;              // TMA descriptor of the field grid (4 x n x (n+7)^2 doubles)
-    bool tma = false;              // fmap encoded (the gather's plane loads use TMA)
     int seg = 8;                   // cells per z-segment work item (set per binning)
     int seg_target = 1024;         // particles per work item the segment length aims at
     double density = 0.0;          // particles per stencil cell at the last binning
@@ -121,7 +110,6 @@ struct Plan {
 void set_error(const std::string &msg);
 int fail_cuda(cudaError_t e, const char *where);
 int fail_cufft(cufftResult r, const char *where);
-void encode_field_tma(Plan &p);   // fields.cu: fills p.fmap / p.tma after the field alloc
 // record the begin (end=false) / end event of a cuFFT exec into the timing ring
 // (no-op unless pif_fft_timing enabled it, and never inside a graph capture)
 void fft_mark(Plan &p, bool z2d, bool end, cudaStream_t s);
