@@ -1282,11 +1282,13 @@ interp_ring_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
     RingStage<W> *stages = reinterpret_cast<RingStage<W> *>(ring_smem);
     RingGather<W> *gathers = reinterpret_cast<RingGather<W> *>(stages + kWarpsPerBlock);
     __shared__ double tab[32];
+    __shared__ int seg_cells[kWarpsPerBlock][kMaxSeg + 1];   // the item's cell boundaries
     if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
     __syncthreads();
     const int lane = threadIdx.x & 31;
     RingStage<W> &st = stages[threadIdx.x >> 5];
     RingGather<W> &rg = gathers[threadIdx.x >> 5];
+    int *cbt = seg_cells[threadIdx.x >> 5];
     const int n = pp.n;
     const double h = pp.h;
     const int64_t M = P.count;
@@ -1309,11 +1311,13 @@ interp_ring_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
         const int ix = col / n, iy = col - ix * n;
         const int k0 = sg * seg, k1 = min(k0 + seg, n);
         const int base = col * n;
-        const int cb = cell_start[base + k0 + min(lane, k1 - k0)];   // seg <= 31
-        const int pbeg = __shfl_sync(kFull, cb, 0) + it.y * kItemParticles;
-        const int pend = min(pbeg + kItemParticles, __shfl_sync(kFull, cb, k1 - k0));
+        __syncwarp();   // the previous item is done with the cell table
+        for (int c = lane; c <= k1 - k0; c += 32) cbt[c] = cell_start[base + k0 + c];
+        __syncwarp();
+        const int pbeg = cbt[0] + it.y * kItemParticles;
+        const int pend = min(pbeg + kItemParticles, cbt[k1 - k0]);
         int kf = k0;
-        while (__shfl_sync(kFull, cb, kf - k0 + 1) <= pbeg) ++kf;
+        while (cbt[kf - k0 + 1] <= pbeg) ++kf;
 
 #pragma unroll 1
         for (int d = 0; d < 3; ++d) {
@@ -1324,7 +1328,7 @@ interp_ring_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                 const int pl = k + ((s - k % W + W) % W);
                 ring_load_plane<W>(g, s, field, d, lane, ix, iy, n, pl % n);
             }
-            int cell_end = __shfl_sync(kFull, cb, k - k0 + 1);
+            int cell_end = cbt[k - k0 + 1];
             double nx = 0.0, ny = 0.0, nz = 0.0;
             if (pbeg + lane < pend) {
                 const int i = perm ? perm[pbeg + lane] : pbeg + lane;
@@ -1342,7 +1346,7 @@ interp_ring_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                     while (pos + j >= cell_end) {   // next cell: plane k leaves, k + W enters
                         ring_load_plane<W>(g, k % W, field, d, lane, ix, iy, n, (k + W) % n);
                         ++k;
-                        cell_end = __shfl_sync(kFull, cb, k - k0 + 1);
+                        cell_end = cbt[k - k0 + 1];
                     }
                     double part = 0.0;
 #pragma unroll
@@ -1702,18 +1706,15 @@ static EsPoly device_poly(const Plan &p) {
 }
 
 // Cells per z-segment work item: 16 at the benchmark density (64 particles per
-// stencil cell); sparser sets get longer segments (up to kMaxSeg; 31 for the
-// ring kernels' one-lane-per-cell start table) so an item still holds
+// stencil cell); sparser sets get longer segments (up to kMaxSeg; the gathers
+// keep an item's cell boundaries in shared memory) so an item still holds
 // ~seg_target particles and the per-item window / first-chunk loads stay
 // amortised.
 int segment_cells(const Plan &p, int64_t M) {
     const double per_cell = (double)M / (double)p.n3;
     const double want = (double)p.seg_target / (per_cell > 1.0 ? per_cell : 1.0);
     const int seg = (int)std::ceil(want);
-    // the ring gather keeps the cell boundaries one per lane (<= 31 cells); the
-    // DMMA gather keeps them in shared memory (<= kMaxSeg)
-    const int cap = (p.w > kMaxFastW || p.force_ring) ? 31 : kMaxSeg;
-    return seg < 8 ? 8 : (seg > cap ? cap : seg);
+    return seg < 8 ? 8 : (seg > kMaxSeg ? kMaxSeg : seg);
 }
 
 int build_items(Plan &p, int64_t M, cudaStream_t s) {
