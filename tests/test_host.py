@@ -204,6 +204,21 @@ def test_deadlock_watchdog():
         pb.spawn_spmd(2, prog, watchdog=0.5)
 
 
+def test_spmd_backend_selection(monkeypatch):
+    """NCCL thread ranks need one GPU per rank; without GPUs (this host) the
+    fixed-order tree rendezvous serves spawn_spmd, and PIF_SPMD_BACKEND or the
+    backend argument pick explicitly."""
+    monkeypatch.delenv("PIF_SPMD_BACKEND", raising=False)
+    assert comm._default_backend(1) == "threads"
+    assert comm._default_backend(4) in ("threads", "nccl")
+    monkeypatch.setenv("PIF_SPMD_BACKEND", "threads")
+    assert comm._default_backend(8) == "threads"
+    seen = pb.spawn_spmd(2, lambda ctx: type(ctx.world.transport).__name__, backend="threads")
+    assert seen == ["ThreadTransport", "ThreadTransport"]
+    with pytest.raises(ValueError):
+        pb.spawn_spmd(2, lambda ctx: None, backend="mpi")
+
+
 def test_p2p_is_outside_this_build():
     with pytest.raises(comm.CommError):
         pb.spawn_spmd(1, lambda ctx: ctx.world.send(0, 1))
