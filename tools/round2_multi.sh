@@ -14,4 +14,16 @@ for n in 2 4; do
     --master-port $((29800 + n)) bench.py --gpus $n --no-cpu-baseline > gpurun_out/r2m_weak_n$n.json \
     2> gpurun_out/r2m_weak_n$n.err
 done
-bash tools/envsweep.sh "--steps 10 --warmup 3" PIF_WEIGHT_CACHE 0 1 > gpurun_out/r2m_wcache.txt 2>&1
+# configs[2]: Penning 64^3, 2^28 particles (strong over 1/2/4 of the 8 GPUs it names)
+for n in 1 2 4; do
+  [ $n -le $G ] || continue
+  if [ $n -eq 1 ]; then
+    python bench.py --kind penning --ppm 1024 --scaling strong --steps 5 --warmup 3 --no-e2e \
+      --no-cpu-baseline > gpurun_out/r2m_penning_n1.json 2> gpurun_out/r2m_penning_n1.err
+  else
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
+      --master-port $((29900 + n)) bench.py --gpus $n --kind penning --ppm 1024 --scaling strong \
+      --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/r2m_penning_n$n.json \
+      2> gpurun_out/r2m_penning_n$n.err
+  fi
+done
