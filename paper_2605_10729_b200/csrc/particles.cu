@@ -1063,17 +1063,31 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
 }
 
 // ----------------------------------------------------------------------------
-// wide windows (9 <= w <= 14): FMA "ring" kernels
+// wide windows (9 <= w <= 17): FMA "ring" kernels
 //
 // Same work items, chunks and cell order as the DMMA kernels, but the w x w
-// (a, b) pairs of the footprint are dealt to the 32 lanes (ceil(w^2/32) per
-// lane) and each lane keeps, per pair, a ring of w z-slots in registers
-// (slot s holds plane z == s mod w of the current cell's footprint).  Per
-// particle of a chunk, lane-owned pairs do acc[t][s] += (s wx[a] wy[b]) wz[s]:
-// w FMAs per pair, all lanes busy, no atomics until a plane leaves the ring.
-// The particle's z weights are stored rotated into slot order by the lane that
-// computes them, so the inner loop has compile-time register indices.
+// (a, b) pairs of the footprint are dealt to the lanes and each lane keeps,
+// per pair, a ring of w z-slots in registers (slot s holds plane z == s mod w
+// of the current cell's footprint).  Per particle of a chunk, lane-owned pairs
+// do acc[t][s] += (s wx[a] wy[b]) wz[s]: w FMAs per pair, all lanes busy, no
+// atomics until a plane leaves the ring.  The particle's z weights are stored
+// rotated into slot order by the lane that computes them, so the inner loop has
+// compile-time register indices.  For w >= 15 (eps <= 1e-14) one warp cannot
+// hold w^2 rings: the pair set is split over G warps ("sub-warps", each
+// claiming (item, part) of the work list), <= 4 pairs per lane; the spread's
+// sub-warps flush their own pairs, the gather's add their partial sums into
+// the per-position scratch and a separate pass pushes.
 // ----------------------------------------------------------------------------
+
+// from this width on the pair set is split over sub-warps (<= 4 pairs per lane)
+#ifndef PIF_RING_SPLIT_W
+#define PIF_RING_SPLIT_W 15
+#endif
+template <int W>
+struct RingSplit {
+    static constexpr int G = W < PIF_RING_SPLIT_W ? 1 : (W * W + 127) / 128;   // sub-warps per item
+    static constexpr int NP = (W * W + 32 * G - 1) / (32 * G);               // pairs per lane
+};
 
 template <int W>
 struct RingStage {
@@ -1081,6 +1095,21 @@ struct RingStage {
     double wy[kChunk][W + 1];   // [p][b]
     double wz[kChunk][W + 1];   // [p][slot]: wz[c] at slot (k_p + c) mod W
 };
+
+// the w window weights of one axis: interior ones by polynomial up to
+// kMaxPolyW, the exact formula (es_weight_fast) for wider windows
+template <int W>
+__device__ __forceinline__ void ring_axis_weights(double c, double beta, const EsPoly &P,
+                                                  const double *tab, double (&wt)[W]) {
+    if (W <= kMaxPolyW) {
+        es_axis_weights<W>(c, beta, P, tab, wt);
+    } else {
+        constexpr double inv_half = 2.0 / W;
+        const double i0 = stencil_start(c, W);
+#pragma unroll
+        for (int a = 0; a < W; ++a) wt[a] = es_weight_fast(c, i0 + (double)a, inv_half, beta, tab);
+    }
+}
 
 // lane p: window weights of its particle into the stage (z rotated by its cell)
 template <int W>
@@ -1090,14 +1119,14 @@ __device__ __forceinline__ void ring_weights(RingStage<W> &st, const double *tab
     if (lane < cnt) {
         // one axis at a time: the ring accumulators stay live across this phase
         double wt[W];
-        es_axis_weights<W>(axis_coord(x, h, rh), beta, P, tab, wt);
+        ring_axis_weights<W>(axis_coord(x, h, rh), beta, P, tab, wt);
 #pragma unroll
         for (int a = 0; a < W; ++a) st.wx[lane][a] = __dmul_rn(sc, wt[a]);
-        es_axis_weights<W>(axis_coord(y, h, rh), beta, P, tab, wt);
+        ring_axis_weights<W>(axis_coord(y, h, rh), beta, P, tab, wt);
 #pragma unroll
         for (int a = 0; a < W; ++a) st.wy[lane][a] = wt[a];
         const double cz = axis_coord(z, h, rh);
-        es_axis_weights<W>(cz, beta, P, tab, wt);
+        ring_axis_weights<W>(cz, beta, P, tab, wt);
         const int r0 = pmod((int)stencil_start(cz, W), n) % W;
 #pragma unroll
         for (int a = 0; a < W; ++a) {
@@ -1108,19 +1137,19 @@ __device__ __forceinline__ void ring_weights(RingStage<W> &st, const double *tab
     __syncwarp();
 }
 
-// plane z (ring slot `slot`) leaves the ring: lane-owned pairs add their
-// value at (ix + a, iy + b, z) and clear the slot
+// plane z (ring slot `slot`) leaves the ring: lane-owned pairs (qbase + lane +
+// 32 t) add their value at (ix + a, iy + b, z) and clear the slot
 template <int W>
-__device__ __forceinline__ void ring_flush_slot(double (&acc)[(W * W + 31) / 32][W], int slot,
-                                                int lane, int ix, int iy, int n, int64_t z,
-                                                double *grid) {
-    constexpr int NP = (W * W + 31) / 32;
+__device__ __forceinline__ void ring_flush_slot(double (&acc)[RingSplit<W>::NP][W], int slot,
+                                                int lane, int qbase, int ix, int iy, int n,
+                                                int64_t z, double *grid) {
+    constexpr int NP = RingSplit<W>::NP;
 #pragma unroll
     for (int s = 0; s < W; ++s) {
         if (s == slot) {
 #pragma unroll
             for (int t = 0; t < NP; ++t) {
-                const int qq = lane + 32 * t;
+                const int qq = qbase + lane + 32 * t;
                 const double v = acc[t][s];
                 if (qq < W * W && v != 0.0) {
                     const int a = qq / W, b = qq - (qq / W) * W;
@@ -1141,44 +1170,49 @@ spread_ring_kernel(const double *__restrict__ px, const double *__restrict__ py,
                    const int32_t *__restrict__ cell_start, double *__restrict__ grid, int n,
                    int seg, int nseg, double h, double beta, const EsPoly poly, unsigned int *work,
                    const int2 *__restrict__ items, const int *__restrict__ n_items) {
-    constexpr int NP = (W * W + 31) / 32;
-    const int nitems = *n_items;
+    constexpr int NP = RingSplit<W>::NP, G = RingSplit<W>::G;
+    const int nunits = *n_items * G;
     const double rh = __drcp_rn(h);
-    __shared__ RingStage<W> stage[kWarpsPerBlock];
+    extern __shared__ double4 ring_spread_smem[];   // RingStage<W> per warp
     __shared__ double tab[32];
+    __shared__ int seg_cells[kWarpsPerBlock][kMaxSeg + 1];   // the item's cell boundaries
     if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    RingStage<W> &st = stage[threadIdx.x >> 5];
-    int pa[NP], pb[NP];
-#pragma unroll
-    for (int t = 0; t < NP; ++t) {
-        const int qq = lane + 32 * t;
-        pa[t] = qq < W * W ? qq / W : 0;
-        pb[t] = qq < W * W ? qq % W : 0;
-    }
+    RingStage<W> &st = reinterpret_cast<RingStage<W> *>(ring_spread_smem)[threadIdx.x >> 5];
+    int *cbt = seg_cells[threadIdx.x >> 5];
 
     for (;;) {
-        int item = 0;
-        if (lane == 0) item = (int)atomicAdd(work, 1u);
-        item = __shfl_sync(kFull, item, 0);
-        if (item >= nitems) break;
+        int unit = 0;
+        if (lane == 0) unit = (int)atomicAdd(work, 1u);
+        unit = __shfl_sync(kFull, unit, 0);
+        if (unit >= nunits) break;
+        const int item = unit / G, qbase = (unit - item * G) * 32 * NP;
+        int pa[NP], pb[NP];
+#pragma unroll
+        for (int t = 0; t < NP; ++t) {
+            const int qq = qbase + lane + 32 * t;
+            pa[t] = qq < W * W ? qq / W : 0;
+            pb[t] = qq < W * W ? qq % W : 0;
+        }
         const int2 it = items[item];
         const int col = it.x / nseg, sg = it.x - col * nseg;
         const int ix = col / n, iy = col - ix * n;
         const int k0 = sg * seg, k1 = min(k0 + seg, n);
         const int base = col * n;
-        const int pbeg = cell_start[base + k0] + it.y * kItemParticles;
-        const int pend = min(pbeg + kItemParticles, cell_start[base + k1]);
+        __syncwarp();   // the previous item is done with the cell table
+        for (int c = lane; c <= k1 - k0; c += 32) cbt[c] = cell_start[base + k0 + c];
+        __syncwarp();
+        const int pbeg = cbt[0] + it.y * kItemParticles;
+        const int pend = min(pbeg + kItemParticles, cbt[k1 - k0]);
         double acc[NP][W];
 #pragma unroll
         for (int t = 0; t < NP; ++t)
 #pragma unroll
             for (int s = 0; s < W; ++s) acc[t][s] = 0.0;
         int k = k0;
-        int cell_end = cell_start[base + k0 + 1];
-        while (cell_end <= pbeg) cell_end = cell_start[base + (++k) + 1];
-        int next_end = cell_start[base + min(k + 2, k1)];
+        int cell_end = cbt[1];
+        while (cell_end <= pbeg) cell_end = cbt[(++k) - k0 + 1];
 
         double nx = 0.0, ny = 0.0, nz = 0.0, ns = q;
         if (pbeg + lane < pend) {
@@ -1202,10 +1236,9 @@ spread_ring_kernel(const double *__restrict__ px, const double *__restrict__ py,
             int j = 0;
             while (j < cnt) {
                 if (pos + j >= cell_end) {   // plane k leaves the ring
-                    ring_flush_slot<W>(acc, k % W, lane, ix, iy, n, k % n, grid);
+                    ring_flush_slot<W>(acc, k % W, lane, qbase, ix, iy, n, k % n, grid);
                     ++k;
-                    cell_end = next_end;
-                    next_end = cell_start[base + min(k + 2, k1)];
+                    cell_end = cbt[k - k0 + 1];
                     continue;
                 }
                 const int jend = min(cnt, cell_end - pos);
@@ -1223,10 +1256,10 @@ spread_ring_kernel(const double *__restrict__ px, const double *__restrict__ py,
             }
             __syncwarp();
         }
-        for (; k < k1; ++k) ring_flush_slot<W>(acc, k % W, lane, ix, iy, n, k % n, grid);
+        for (; k < k1; ++k) ring_flush_slot<W>(acc, k % W, lane, qbase, ix, iy, n, k % n, grid);
         // planes k1 .. k1 + W - 2 are still in the ring
         for (int pl = k1; pl < k1 + W - 1; ++pl)
-            ring_flush_slot<W>(acc, pl % W, lane, ix, iy, n, pl % n, grid);
+            ring_flush_slot<W>(acc, pl % W, lane, qbase, ix, iy, n, pl % n, grid);
     }
 }
 
@@ -1236,24 +1269,25 @@ spread_ring_kernel(const double *__restrict__ px, const double *__restrict__ py,
 // swapped per cell step); per particle a lane forms
 // sum_t wx[a_t] wy[b_t] sum_s E_d[t][s] wz[s], the 32 lane partials are reduced
 // per particle through shared memory and E_d goes to a per-position scratch
-// (L2-resident).  A last walk pushes every particle exactly as
-// interp_mma_kernel does.  Window weights are recomputed per component walk.
+// (L2-resident; added to by each sub-warp when G > 1).  A last walk pushes every
+// particle exactly as interp_mma_kernel does (for G > 1 in ring_push_kernel,
+// after all sub-warps are done).  Window weights are recomputed per component walk.
 template <int W>
 struct RingGather {
     double red[kChunk][kChunk + 1];   // [particle][lane] partial sums
 };
 
 template <int W>
-__device__ __forceinline__ void ring_load_plane(double (&g)[(W * W + 31) / 32][W], int slot,
-                                                const double4 *field, int comp, int lane, int ix,
-                                                int iy, int n, int64_t z) {
-    constexpr int NP = (W * W + 31) / 32;
+__device__ __forceinline__ void ring_load_plane(double (&g)[RingSplit<W>::NP][W], int slot,
+                                                const double4 *field, int comp, int lane,
+                                                int qbase, int ix, int iy, int n, int64_t z) {
+    constexpr int NP = RingSplit<W>::NP;
 #pragma unroll
     for (int s = 0; s < W; ++s) {
         if (s == slot) {
 #pragma unroll
             for (int t = 0; t < NP; ++t) {
-                const int qq = lane + 32 * t;
+                const int qq = qbase + lane + 32 * t;
                 double v = 0.0;
                 if (qq < W * W) {
                     const int a = qq / W, b = qq - (qq / W) * W;
@@ -1267,6 +1301,35 @@ __device__ __forceinline__ void ring_load_plane(double (&g)[(W * W + 31) / 32][W
     }
 }
 
+// push of the particle at cell-order position pos with its gathered E
+template <bool PUSH>
+__device__ __forceinline__ void ring_push_one(const pif_soa_t &P, const int32_t *perm,
+                                              const pif_soa_t &Q, const PushParams &pp, int64_t pos,
+                                              double E0, double E1, double E2, int32_t *key,
+                                              int32_t *rank, int32_t *count, double *E_out,
+                                              double (&dg)[5]) {
+    const int64_t i = perm ? perm[pos] : pos;
+    if (PUSH) {
+        double x = P.x[i], y = P.y[i], z = P.z[i];
+        double vx = P.vx[i], vy = P.vy[i], vz = P.vz[i];
+        const int64_t id = P.id[i];
+        boris_one(pp, E0, E1, E2, x, y, z, vx, vy, vz, dg);
+        Q.x[pos] = x; Q.y[pos] = y; Q.z[pos] = z;
+        Q.vx[pos] = vx; Q.vy[pos] = vy; Q.vz[pos] = vz;
+        Q.id[pos] = id;
+        mirror_store(pp, id, x, y, z, vx, vy, vz);
+        const int kk = cell_key(x, y, z, pp.h, pp.rh, pp.w, pp.n);
+        key[pos] = kk;
+        if (rank) rank[pos] = atomicAdd(&count[kk], 1);
+        else atomicAdd(&count[kk], 1);
+    } else {
+        const int64_t o = 3 * P.id[i];
+        E_out[o] = E0;
+        E_out[o + 1] = E1;
+        E_out[o + 2] = E2;
+    }
+}
+
 template <int W, bool PUSH>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
 interp_ring_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
@@ -1276,8 +1339,8 @@ interp_ring_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                    int32_t *__restrict__ count, double *__restrict__ partials,
                    double *__restrict__ E_out, double *__restrict__ scratch, unsigned int *work,
                    const int2 *__restrict__ items, const int *__restrict__ n_items) {
-    constexpr int NP = (W * W + 31) / 32;
-    const int nitems = *n_items;
+    constexpr int NP = RingSplit<W>::NP, G = RingSplit<W>::G;
+    const int nunits = *n_items * G;
     extern __shared__ double4 ring_smem[];
     RingStage<W> *stages = reinterpret_cast<RingStage<W> *>(ring_smem);
     RingGather<W> *gathers = reinterpret_cast<RingGather<W> *>(stages + kWarpsPerBlock);
@@ -1292,20 +1355,21 @@ interp_ring_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
     const int n = pp.n;
     const double h = pp.h;
     const int64_t M = P.count;
-    int pa[NP], pb[NP];
-#pragma unroll
-    for (int t = 0; t < NP; ++t) {
-        const int qq = lane + 32 * t;
-        pa[t] = qq < W * W ? qq / W : 0;
-        pb[t] = qq < W * W ? qq % W : 0;
-    }
     double dg[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 
     for (;;) {
-        int item = 0;
-        if (lane == 0) item = (int)atomicAdd(work, 1u);
-        item = __shfl_sync(kFull, item, 0);
-        if (item >= nitems) break;
+        int unit = 0;
+        if (lane == 0) unit = (int)atomicAdd(work, 1u);
+        unit = __shfl_sync(kFull, unit, 0);
+        if (unit >= nunits) break;
+        const int item = unit / G, qbase = (unit - item * G) * 32 * NP;
+        int pa[NP], pb[NP];
+#pragma unroll
+        for (int t = 0; t < NP; ++t) {
+            const int qq = qbase + lane + 32 * t;
+            pa[t] = qq < W * W ? qq / W : 0;
+            pb[t] = qq < W * W ? qq % W : 0;
+        }
         const int2 it = items[item];
         const int col = it.x / nseg, sg = it.x - col * nseg;
         const int ix = col / n, iy = col - ix * n;
@@ -1326,7 +1390,7 @@ interp_ring_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
 #pragma unroll
             for (int s = 0; s < W; ++s) {   // planes k .. k + W - 1 of the first cell
                 const int pl = k + ((s - k % W + W) % W);
-                ring_load_plane<W>(g, s, field, d, lane, ix, iy, n, pl % n);
+                ring_load_plane<W>(g, s, field, d, lane, qbase, ix, iy, n, pl % n);
             }
             int cell_end = cbt[k - k0 + 1];
             double nx = 0.0, ny = 0.0, nz = 0.0;
@@ -1344,7 +1408,8 @@ interp_ring_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                 ring_weights<W>(st, tab, poly, lane, cnt, x0, y0, z0, 1.0, h, pp.rh, beta, n);
                 for (int j = 0; j < cnt; ++j) {
                     while (pos + j >= cell_end) {   // next cell: plane k leaves, k + W enters
-                        ring_load_plane<W>(g, k % W, field, d, lane, ix, iy, n, (k + W) % n);
+                        ring_load_plane<W>(g, k % W, field, d, lane, qbase, ix, iy, n,
+                                           (k + W) % n);
                         ++k;
                         cell_end = cbt[k - k0 + 1];
                     }
@@ -1363,37 +1428,35 @@ interp_ring_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                     double e = 0.0;
 #pragma unroll 8
                     for (int l = 0; l < 32; ++l) e += rg.red[lane][l];
-                    scratch[d * M + pos + lane] = e;
+                    if (G == 1) scratch[d * M + pos + lane] = e;
+                    else atomicAdd(&scratch[d * M + pos + lane], e);   // two or three adds
                 }
                 __syncwarp();
             }
         }
-        // push walk (the lane reads back its own scratch entries)
-        for (int pos = pbeg + lane; pos < pend; pos += 32) {
-            const int i = perm ? perm[pos] : pos;
-            const double E0 = scratch[pos], E1 = scratch[M + pos], E2 = scratch[2 * M + pos];
-            if (PUSH) {
-                double x = P.x[i], y = P.y[i], z = P.z[i];
-                double vx = P.vx[i], vy = P.vy[i], vz = P.vz[i];
-                const int64_t id = P.id[i];
-                boris_one(pp, E0, E1, E2, x, y, z, vx, vy, vz, dg);
-                Q.x[pos] = x; Q.y[pos] = y; Q.z[pos] = z;
-                Q.vx[pos] = vx; Q.vy[pos] = vy; Q.vz[pos] = vz;
-                Q.id[pos] = id;
-                mirror_store(pp, id, x, y, z, vx, vy, vz);
-                const int kk = cell_key(x, y, z, h, pp.rh, pp.w, n);
-                key[pos] = kk;
-                if (rank) rank[pos] = atomicAdd(&count[kk], 1);
-                else atomicAdd(&count[kk], 1);
-            } else {
-                const int64_t o = 3 * P.id[i];
-                E_out[o] = E0;
-                E_out[o + 1] = E1;
-                E_out[o + 2] = E2;
-            }
+        if (G == 1) {   // push walk (the lane reads back its own scratch entries)
+            for (int pos = pbeg + lane; pos < pend; pos += 32)
+                ring_push_one<PUSH>(P, perm, Q, pp, pos, scratch[pos], scratch[M + pos],
+                                    scratch[2 * M + pos], key, rank, count, E_out, dg);
+            __syncwarp();
         }
-        __syncwarp();
     }
+    if (PUSH && G == 1) block_diag_store(dg, partials);
+}
+
+// push (or E output) of every position after a split (G > 1) ring gather
+template <bool PUSH>
+__global__ void ring_push_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
+                                 PushParams pp, int32_t *__restrict__ key,
+                                 int32_t *__restrict__ rank, int32_t *__restrict__ count,
+                                 double *__restrict__ partials, double *__restrict__ E_out,
+                                 const double *__restrict__ scratch) {
+    const int64_t M = P.count;
+    double dg[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int64_t pos = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pos < M;
+         pos += (int64_t)gridDim.x * blockDim.x)
+        ring_push_one<PUSH>(P, perm, Q, pp, pos, scratch[pos], scratch[M + pos],
+                            scratch[2 * M + pos], key, rank, count, E_out, dg);
     if (PUSH) block_diag_store(dg, partials);
 }
 
@@ -1616,7 +1679,10 @@ constexpr double kRingGatherMinDensity = 2.0;
 constexpr double kRingSpreadMinDensity = 0.75;
 
 bool ring_path_ok(const Plan &p) {
-    if (p.force_generic || p.poly.exact_mask != 0) return false;
+    if (p.force_generic) return false;
+    // w <= kMaxPolyW evaluates interior weights by polynomial (all must pass
+    // the plan's accuracy check); wider windows use the exact formula
+    if (p.w <= kMaxPolyW && p.poly.exact_mask != 0) return false;
     return (p.w >= 9 && p.w <= kMaxRingW) || (p.force_ring && p.w == 8);
 }
 
@@ -1926,8 +1992,10 @@ int launch_spread(Plan &p, const pif_soa_t &P, const int32_t *perm, const double
 #define PIF_RING_SPREAD_CASE(W)                                                              \
     case W: {                                                                                \
         auto k = spread_ring_kernel<W>;                                                     \
-        int blocks = persistent_blocks(k, threads, 0, p.sm_count);                           \
-        k<<<blocks, threads, 0, s>>>(P.x, P.y, P.z, P.id, perm, strengths, q, p.cell_start,   \
+        const int dyn = (int)(kWarpsPerBlock * sizeof(RingStage<W>));                        \
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);           \
+        int blocks = persistent_blocks(k, threads, dyn, p.sm_count);                         \
+        k<<<blocks, threads, dyn, s>>>(P.x, P.y, P.z, P.id, perm, strengths, q, p.cell_start, \
                                      p.grid, p.n, p.seg, nseg, p.h, p.beta, poly, p.work,     \
                                      p.items, nitems);                                       \
         break;                                                                               \
@@ -1940,6 +2008,9 @@ int launch_spread(Plan &p, const pif_soa_t &P, const int32_t *perm, const double
             PIF_RING_SPREAD_CASE(12)
             PIF_RING_SPREAD_CASE(13)
             PIF_RING_SPREAD_CASE(14)
+            PIF_RING_SPREAD_CASE(15)
+            PIF_RING_SPREAD_CASE(16)
+            PIF_RING_SPREAD_CASE(17)
             default:
                 set_error("unsupported window width");
                 return PIF_ERR_VALUE;
@@ -2052,6 +2123,11 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
     case W: {                                                                                 \
         const size_t dyn = kWarpsPerBlock * (sizeof(RingStage<W>) + sizeof(RingGather<W>));   \
         if (ensure_ring_scratch(p, P.count) != PIF_OK) return PIF_ERR_CUDA;                    \
+        constexpr bool split = RingSplit<W>::G > 1;                                           \
+        if (split) {   /* sub-warps add their partials into the scratch */                    \
+            e = cudaMemsetAsync(p.ring_scratch, 0, sizeof(double) * 3 * P.count, s);          \
+            if (e != cudaSuccess) return fail_cuda(e, "zero ring scratch");                    \
+        }                                                                                     \
         auto k = push ? interp_ring_kernel<W, true> : interp_ring_kernel<W, false>;           \
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);       \
         blocks = persistent_blocks(k, threads, dyn, p.sm_count);                              \
@@ -2059,6 +2135,13 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
         k<<<blocks, threads, dyn, s>>>(P, perm, Q, p.cell_start, field, p.seg, nseg, p.beta,   \
                                        poly, pp, key, rank, p.cell_count, p.partials, E_out,  \
                                        p.ring_scratch, p.work, p.items, nitems);              \
+        if (split) {                                                                          \
+            blocks = grid_for(P.count, 128, p.sm_count);                                      \
+            if (blocks > p.partial_blocks) blocks = p.partial_blocks;                         \
+            auto kp = push ? ring_push_kernel<true> : ring_push_kernel<false>;                \
+            kp<<<blocks, 128, 0, s>>>(P, perm, Q, pp, key, rank, p.cell_count, p.partials,    \
+                                      E_out, p.ring_scratch);                                 \
+        }                                                                                     \
         break;                                                                                \
     }
         switch (p.w) {
@@ -2069,6 +2152,9 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
             PIF_RING_INTERP_CASE(12)
             PIF_RING_INTERP_CASE(13)
             PIF_RING_INTERP_CASE(14)
+            PIF_RING_INTERP_CASE(15)
+            PIF_RING_INTERP_CASE(16)
+            PIF_RING_INTERP_CASE(17)
             default:
                 set_error("unsupported window width");
                 return PIF_ERR_VALUE;

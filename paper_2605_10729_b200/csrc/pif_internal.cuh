@@ -24,7 +24,7 @@ namespace pif {
 // windows (eps < 1e-8) take the generic one-thread-per-particle path.
 constexpr int kMaxFastW = 8;    // DMMA kernels
 constexpr int kMaxPolyW = 14;   // polynomial weights: pair rows a <= 6 (EsPoly)
-constexpr int kMaxRingW = 14;   // FMA ring kernels (register ring of w slots per lane pair)
+constexpr int kMaxRingW = 17;   // FMA ring kernels (register ring of w slots per lane pair)
 constexpr int kMaxW = 17;          // eps >= 1e-16 (nufft.py:74)
 constexpr int kSub = 8;            // particles per warp sub-batch (fast kernels)
 constexpr int kWarpsPerBlock = 4;  // fast kernels: one work item per warp
