@@ -599,15 +599,20 @@ def test_run_host_streaming_matches_pif_step(cuda):
     assert np.all(np.isfinite(wh.numpy())) and np.all(wh.numpy() > 0)
 
 
-@pytest.mark.parametrize("eps", [1e-9, 1e-12])
-def test_wide_window_ring_kernels_match_oracle(eps):
-    """w = 10 / 13 at ~5 particles per stencil cell: the FMA ring spreader and
-    gather (+ push via pif_step) against the oracle."""
+@pytest.mark.parametrize("eps,N,M", [(1e-9, 8, 20000), (1e-12, 8, 20000), (1e-13, 12, 70000),
+                                     (1e-14, 12, 70000), (1e-15, 12, 70000),
+                                     (1e-16, 12, 70000)])
+def test_wide_window_ring_kernels_match_oracle(eps, N, M):
+    """w = 10 / 13 / 14 (one warp per ring) and 15 / 16 / 17 (pair set split
+    over sub-warps, split gather + second push pass) at ~5 particles per
+    stencil cell: the FMA ring spreader and gather (+ push via pif_step)
+    against the oracle."""
     o = oracle()
-    N, L, M = 8, 4 * np.pi, 20000
+    L = 4 * np.pi
     plan = pb.make_plan(N, L, eps)
     op = o.make_plan(N, L, eps)
-    assert plan.window.w in (10, 13)
+    assert plan.window.w == {1e-9: 10, 1e-12: 13, 1e-13: 14, 1e-14: 15, 1e-15: 16,
+                             1e-16: 17}[eps]
     rng = np.random.default_rng(11)
     x = rng.random((M, 3)) * L
     v = rng.standard_normal((M, 3))
