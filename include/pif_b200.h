@@ -245,6 +245,14 @@ int pif_probe_fp64(double *scratch, int blocks, int threads, int iters, void *st
 int pif_set_deterministic(pif_plan_t plan, int enable);
 int pif_is_deterministic(pif_plan_t plan);
 
+/* 1 if the gather+push counts next-cell keys per run of equal keys in dense
+ * segments (sets with heavy cells, e.g. a Penning cloud at 2^28 on one GPU),
+ * 0 for per-particle counts.  Decided at the first binning after each
+ * pif_bin_keys / pif_load_aos from the most particles any z-segment holds
+ * (>= 12 work items); PIF_PUSH_AGG=0/1 in the environment forces it.  Same
+ * counts either way: a performance switch only. */
+int pif_push_aggregated(pif_plan_t plan);
+
 /* ---- in-process communicators: replaces comm.allreduce_sum's fixed-order
  * tree over rank threads (comm.py:329-339, 391-408) for spawn_spmd's thread
  * ranks (comm.py:483-528), one GPU per rank.

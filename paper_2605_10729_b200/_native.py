@@ -84,6 +84,7 @@ SIGNATURES = {
     "pif_sample_landau_axis": ([_P, _P, _I64, _I64, _D, _D, _D, _P, _I64, _P, _P], _I),
     "pif_set_deterministic": ([_P, _I], _I),
     "pif_is_deterministic": ([_P], _I),
+    "pif_push_aggregated": ([_P], _I),
     "pif_nccl_version": ([ctypes.POINTER(ctypes.c_int)], _I),
     "pif_comm_init_all": ([_I, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_P)], _I),
     "pif_allreduce_f64": ([_P, _P, _I64, _P], _I),

@@ -54,7 +54,7 @@ int dalloc(Plan &p, T **ptr, size_t count) {
 void release(Plan &p) {
     void *ptrs[] = {p.deconv, p.kvec, p.grid, p.spec, p.field, p.field3, p.emodes, p.cgrid,
                     p.cell_count, p.cell_start, p.scan_tmp, p.work, p.partials, p.maxbits,
-                    p.shape_tab, p.items, p.seg_parts, p.seg_off, p.ring_scratch, p.wcache,
+                    p.shape_tab, p.items, p.seg_parts, p.seg_off, p.max_parts, p.ring_scratch, p.wcache,
                     p.dbuf, p.det_keys, p.det_iota, p.det_tmp};
     for (void *q : ptrs)
         if (q) cudaFree(q);
@@ -210,6 +210,9 @@ int pif_plan_create(const pif_plan_desc_t *d, int device, pif_plan_t *out) {
     if (const char *fg = std::getenv("PIF_FORCE_GENERIC")) p.force_generic = std::atoi(fg) != 0;
     if (const char *st = std::getenv("PIF_SEG_TARGET")) p.seg_target = std::max(1, std::atoi(st));
     if (const char *fr = std::getenv("PIF_FORCE_RING")) p.force_ring = std::atoi(fr) != 0;
+    if (const char *pa = std::getenv("PIF_PUSH_AGG")) p.push_agg_force = std::atoi(pa) != 0;
+    if (const char *rs = std::getenv("PIF_RING_SPREAD_MIN")) p.ring_spread_min = std::atof(rs);
+    if (const char *rg = std::getenv("PIF_RING_GATHER_MIN")) p.ring_gather_min = std::atof(rg);
     int rc = PIF_OK;
 #define TRY(x)                    \
     do {                          \
@@ -229,6 +232,7 @@ int pif_plan_create(const pif_plan_desc_t *d, int device, pif_plan_t *out) {
     p.n_segs = p.n * p.n * ((p.n + p.seg - 1) / p.seg);
     TRY(pif::dalloc(p, &p.seg_parts, p.n_segs + 1));
     TRY(pif::dalloc(p, &p.seg_off, p.n_segs + 1));
+    TRY(pif::dalloc(p, &p.max_parts, 1));
     TRY(pif::dalloc(p, &p.partials, (size_t)p.partial_blocks * pif::kDiagSlots));
     TRY(pif::dalloc(p, &p.maxbits, 8));
     {
@@ -338,6 +342,7 @@ int pif_bin_keys(pif_plan_t plan, const pif_soa_t *src, int32_t *key, int32_t *r
     PLAN_CHECK();
     if (!pif::soa_ok(src, false)) return pif::bad("invalid particle view");
     if (src->count > 0 && (!key || !rank)) return pif::bad("missing key/rank buffers");
+    p.agg_check = true;   // a new particle set: re-decide push_agg at its binning
     return pif::launch_bin_keys(p, *src, key, rank, s);
 }
 
@@ -408,6 +413,8 @@ int pif_set_deterministic(pif_plan_t plan, int enable) {
 }
 
 int pif_is_deterministic(pif_plan_t plan) { return plan && plan->p.det ? 1 : 0; }
+
+int pif_push_aggregated(pif_plan_t plan) { return plan && plan->p.push_agg ? 1 : 0; }
 
 int pif_fft_timing(pif_plan_t plan, int slots) {
     if (!plan) return pif::bad("null plan");
@@ -565,6 +572,7 @@ int pif_load_aos(pif_plan_t plan, const double *x, const double *v, int64_t id0,
     PLAN_CHECK();
     if (!pif::soa_ok(dst, true)) return pif::bad("invalid destination view");
     if (dst->count > 0 && (!x || !key)) return pif::bad("missing input / key");
+    p.agg_check = true;
     return pif::launch_load_aos(p, x, v, id0, *dst, key, rank, s);
 }
 

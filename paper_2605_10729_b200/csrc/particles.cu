@@ -204,6 +204,15 @@ __global__ void seg_items_kernel(const int *__restrict__ parts, const int *__res
     }
 }
 
+__global__ void max_parts_kernel(const int *__restrict__ parts, int nsegs, int *out) {
+    int m = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nsegs; i += gridDim.x * blockDim.x)
+        m = max(m, parts[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(out, m);
+}
+
 // ----------------------------------------------------------------------------
 // DMMA building blocks
 // ----------------------------------------------------------------------------
@@ -840,8 +849,11 @@ constexpr int kGatherWarps = PIF_GATHER_WARPS;   // warps per gather block
 
 // WC: the window weights come from the spread's cache (pif_set_weight_cache)
 // instead of being evaluated here; a separate instantiation so the polynomial
-// code and its registers are not carried when unused.
-template <int W, bool PUSH, bool LONGSEG, bool WC>
+// code and its registers are not carried when unused.  AGG (Plan::push_agg,
+// sets with heavy cells): dense segments count next-cell keys per run of
+// equal keys; its own instantiation for the same reason (+9 registers, 2%
+// slower where per-lane REDs do not collide).
+template <int W, bool PUSH, bool LONGSEG, bool WC, bool AGG>
 __global__ void __launch_bounds__(kGatherWarps * 32, WC ? PIF_INTERP_MINB_WC : PIF_INTERP_MINB)
 interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                   const int32_t *__restrict__ cell_start,
@@ -909,6 +921,12 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
         auto bound = [&](int t) { return LONGSEG ? cbt[t] : __shfl_sync(kFull, cb, t); };
         const int pbeg = bound(0) + it.y * kItemParticles;
         const int pend = min(pbeg + kItemParticles, bound(k1 - k0));
+        // dense segment (> 3 parts, so several warps push into the same few
+        // cells at once): one count RED per run of equal next-cell keys in
+        // lane order instead of one per particle.  Per-lane REDs to one
+        // address serialise in L2 (Penning 2^28 per GPU: gather 57.6 ->
+        // 34.3 ms); at 64 per cell they are cheaper than the warp exchange.
+        const bool agg = AGG && PUSH && !rank && bound(k1 - k0) - bound(0) > 3 * kItemParticles;
         int kf = k0;   // cell holding the item's first particle
         while (bound(kf - k0 + 1) <= pbeg) ++kf;
         const int64_t yrow = (iy + r) % n;
@@ -1011,6 +1029,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
             __syncwarp();
             PHASE_MARK(t2);
             PHASE_ADD(1, t1, t2);
+            int ckey = -1;   // next cell key to count (dense segments)
             if (lane < cnt) {
                 const int64_t i = pos + lane;
                 double Eg[3];
@@ -1033,14 +1052,26 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                     } else {
                         // count only (RED, nothing returns): pif_bin_perm
                         // assigns the in-cell slots, so no atomic round trip
-                        // sits on this warp's scoreboards
-                        atomicAdd(&count[kk], 1);
+                        // sits on this warp's scoreboards.  Dense segments
+                        // count per run of equal keys after the lane branch.
+                        if (agg) ckey = kk;
+                        else atomicAdd(&count[kk], 1);
                     }
                 } else {
                     const int64_t o = 3 * id0;
                     E_out[o] = E0;
                     E_out[o + 1] = E1;
                     E_out[o + 2] = E2;
+                }
+            }
+            if (AGG && PUSH && agg) {
+                const int prev_k = __shfl_up_sync(kFull, ckey, 1);
+                const bool head = ckey >= 0 && (lane == 0 || prev_k != ckey);
+                const unsigned heads = __ballot_sync(kFull, lane == 0 || prev_k != ckey);
+                if (head) {
+                    const unsigned later = heads & ~((2u << lane) - 1u);
+                    const int end = later ? __ffs(later) - 1 : cnt;
+                    atomicAdd(&count[ckey], end - lane);
                 }
             }
             __syncwarp();
@@ -1072,8 +1103,10 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
 // do acc[t][s] += (s wx[a] wy[b]) wz[s]: w FMAs per pair, all lanes busy, no
 // atomics until a plane leaves the ring.  The particle's z weights are stored
 // rotated into slot order by the lane that computes them, so the inner loop has
-// compile-time register indices.  For w >= 15 (eps <= 1e-14) one warp cannot
-// hold w^2 rings: the pair set is split over G warps ("sub-warps", each
+// compile-time register indices.  From w = 13 (eps <= 1e-12) one warp does
+// not hold w^2 rings without spilling (w = 13 / 14 unsplit: 200-600 B of
+// spills; split vs unsplit A/B in profiles/round2/ring_split_ab.txt), from
+// w = 15 not at all: the pair set is split over G warps ("sub-warps", each
 // claiming (item, part) of the work list), <= 4 pairs per lane; the spread's
 // sub-warps flush their own pairs, the gather's add their partial sums into
 // the per-position scratch and a separate pass pushes.
@@ -1081,7 +1114,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
 
 // from this width on the pair set is split over sub-warps (<= 4 pairs per lane)
 #ifndef PIF_RING_SPLIT_W
-#define PIF_RING_SPLIT_W 15
+#define PIF_RING_SPLIT_W 13
 #endif
 template <int W>
 struct RingSplit {
@@ -1671,12 +1704,14 @@ int ensure_ring_scratch(Plan &p, int64_t M) {
     return PIF_OK;
 }
 
-// below ~2 particles per stencil cell the ring gather reloads a plane per
-// particle and the one-thread-per-particle gather is faster
-constexpr double kRingGatherMinDensity = 2.0;
-// the ring spreader flushes w^2 values per plane it passes: below ~1 particle
-// per cell the one-thread-per-particle atomics are cheaper
-constexpr double kRingSpreadMinDensity = 0.75;
+// Density thresholds of the ring kernels (Plan::ring_spread_min = 0,
+// ring_gather_min = 0.75 particles per stencil cell).  With segments of up to
+// 127 cells and zero planes skipped, the ring spreader beats the
+// one-thread-per-particle atomics at every density measured (0.125 per cell:
+// 2.3x / 1.9x at w = 13 / 10); the ring gather, which reloads a plane per cell
+// step, wins from ~1 per cell (1.5x / 2.5x) and loses below (0.5 per cell:
+// -6% / -45% at w = 13 / 16; 0.125: -90% / -40% at w = 13 / 10).
+// profiles/round2/ring_density_ab.txt
 
 bool ring_path_ok(const Plan &p) {
     if (p.force_generic) return false;
@@ -1804,7 +1839,31 @@ int build_items(Plan &p, int64_t M, cudaStream_t s) {
     if (e != cudaSuccess) return fail_cuda(e, "segment scan");
     seg_items_kernel<<<grid_for(p.n_segs, 256, p.sm_count), 256, 0, s>>>(p.seg_parts, p.seg_off,
                                                                          p.n_segs, p.items);
-    return fail_cuda(cudaGetLastError(), "work item kernels");
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return fail_cuda(e, "work item kernels");
+    if (p.push_agg_force >= 0) {
+        p.push_agg = p.push_agg_force != 0;
+    } else if (p.agg_check) {
+        // once per particle set, outside graph capture: the most parts any
+        // segment holds (Landau 64^3 / 2^27: 2; Penning 2^28 on one GPU: dozens)
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        e = cudaStreamIsCapturing(s, &cs);
+        if (e != cudaSuccess) return fail_cuda(e, "capture status");
+        if (cs == cudaStreamCaptureStatusNone) {
+            int mp = 0;
+            e = cudaMemsetAsync(p.max_parts, 0, sizeof(int), s);
+            if (e == cudaSuccess) {
+                max_parts_kernel<<<grid_for(p.n_segs, 256, p.sm_count), 256, 0, s>>>(
+                    p.seg_parts, p.n_segs, p.max_parts);
+                e = cudaMemcpyAsync(&mp, p.max_parts, sizeof(int), cudaMemcpyDeviceToHost, s);
+            }
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) return fail_cuda(e, "max parts per segment");
+            p.push_agg = mp >= kPushAggMinParts;
+            p.agg_check = false;
+        }
+    }
+    return PIF_OK;
 }
 
 int launch_soa_to_aos(Plan &p, const pif_soa_t &P, int64_t id0, double *ox, double *ov,
@@ -1983,7 +2042,7 @@ int launch_spread(Plan &p, const pif_soa_t &P, const int32_t *perm, const double
             det_reduce_kernel<<<grid_for(p.n3, 256, p.sm_count), 256, 0, s>>>(
                 p.dbuf, det.stride, p.seg_off, p.seg_parts, p.n, p.seg, nseg, p.w, p.grid);
         }
-    } else if (ring_path_ok(p) && p.density >= kRingSpreadMinDensity) {
+    } else if (ring_path_ok(p) && p.density >= p.ring_spread_min) {
         const int nseg = (p.n + p.seg - 1) / p.seg;
         const int *nitems = p.seg_off + p.n_segs;
         e = cudaMemsetAsync(p.work, 0, sizeof(unsigned int), s);
@@ -2073,10 +2132,12 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
 #define PIF_INTERP_CASE(W)                                                                    \
     case W: {                                                                                 \
         if (push) {                                                                           \
-            auto k = longseg ? (wc ? interp_mma_kernel<W, true, true, true>                   \
-                                   : interp_mma_kernel<W, true, true, false>)                 \
-                             : (wc ? interp_mma_kernel<W, true, false, true>                  \
-                                   : interp_mma_kernel<W, true, false, false>);               \
+            auto k = longseg ? (wc ? interp_mma_kernel<W, true, true, true, false>            \
+                                   : interp_mma_kernel<W, true, true, false, false>)          \
+                   : p.push_agg ? (wc ? interp_mma_kernel<W, true, false, true, true>          \
+                                      : interp_mma_kernel<W, true, false, false, true>)       \
+                                : (wc ? interp_mma_kernel<W, true, false, true, false>         \
+                                      : interp_mma_kernel<W, true, false, false, false>);     \
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kGatherDynMax); \
             blocks = persistent_blocks(k, gthreads, dyn, p.sm_count);                         \
             if (blocks > p.partial_blocks) blocks = p.partial_blocks;                         \
@@ -2086,10 +2147,10 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
                                          key, rank, p.cell_count, p.partials, E_out, p.work,   \
                                          p.items, nitems, wc, P.count);                       \
         } else {                                                                              \
-            auto k = longseg ? (wc ? interp_mma_kernel<W, false, true, true>                  \
-                                   : interp_mma_kernel<W, false, true, false>)                \
-                             : (wc ? interp_mma_kernel<W, false, false, true>                 \
-                                   : interp_mma_kernel<W, false, false, false>);              \
+            auto k = longseg ? (wc ? interp_mma_kernel<W, false, true, true, false>           \
+                                   : interp_mma_kernel<W, false, true, false, false>)         \
+                             : (wc ? interp_mma_kernel<W, false, false, true, false>          \
+                                   : interp_mma_kernel<W, false, false, false, false>);       \
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kGatherDynMax); \
             blocks = persistent_blocks(k, gthreads, dyn, p.sm_count);                         \
             k<<<blocks, gthreads, dyn, s>>>(P, perm, Q, p.cell_start, field, p.seg, nseg,     \
@@ -2113,7 +2174,7 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
                 return PIF_ERR_VALUE;
         }
 #undef PIF_INTERP_CASE
-    } else if (P.count > 0 && ring_path_ok(p) && p.density >= kRingGatherMinDensity) {
+    } else if (P.count > 0 && ring_path_ok(p) && p.density >= p.ring_gather_min) {
         const int nseg = (p.n + p.seg - 1) / p.seg;
         const int *nitems = p.seg_off + p.n_segs;
         e = cudaMemsetAsync(p.work, 0, sizeof(unsigned int), s);

@@ -30,6 +30,10 @@ constexpr int kSub = 8;            // particles per warp sub-batch (fast kernels
 constexpr int kWarpsPerBlock = 4;  // fast kernels: one work item per warp
 constexpr int kDiagSlots = 6;
 constexpr int kItemParticles = 1024;   // max particles per work item
+// push_agg from this many parts in the densest segment (A/B: Landau at 64 / 512
+// per cell, 2 / 4 parts: per-lane REDs 2% faster; Penning 2^28 on one GPU,
+// dozens of parts: aggregated counts 1.7x faster)
+constexpr int kPushAggMinParts = 12;
 constexpr int kMaxSeg = 127;           // max cells per z-segment work item (DMMA kernels)
 
 // polynomial coefficients for the interior window weights (es_fast.cuh)
@@ -46,6 +50,8 @@ struct Plan {
     int64_t n3 = 0, nhalf = 0;     // n^3, n*n*(n/2+1)
     int seg = 8;                   // cells per z-segment work item (set per binning)
     int seg_target = 1024;         // particles per work item the segment length aims at
+    double ring_spread_min = 0.0;   // ring kernels from this many particles per stencil cell
+    double ring_gather_min = 0.75;  // (PIF_RING_SPREAD_MIN / PIF_RING_GATHER_MIN override, A/B)
     double density = 0.0;          // particles per stencil cell at the last binning
     double *ring_scratch = nullptr;  // E per position for the wide-window gather
     bool wcache_on = false;        // spread keeps its window weights for the next gather
@@ -78,6 +84,15 @@ struct Plan {
     int64_t items_cap = 0;
     int *seg_parts = nullptr;      // n_segs + 1
     int *seg_off = nullptr;        // n_segs + 1; seg_off[n_segs] = number of items
+    int *max_parts = nullptr;      // (1) most parts in one segment (push_agg decision)
+    // push_agg: the gather+push kernel counts next-cell keys per run of equal
+    // keys in dense segments instead of per particle (heavy cells: per-lane
+    // REDs to one counter serialise in L2).  Decided from the parts per
+    // segment at the first binning after a load (agg_check; never inside a
+    // graph capture); PIF_PUSH_AGG=0/1 forces it.
+    bool push_agg = false;
+    bool agg_check = true;
+    int push_agg_force = -1;
     int n_segs = 0;
     double *partials = nullptr;    // per-block diagnostic / reduction partials
     int partial_blocks = 0;

@@ -87,6 +87,12 @@ class PifEngine:
             _native.call("pif_set_weight_cache", self.handle, 0)
             self.weight_cache = False
 
+    @property
+    def push_aggregated(self) -> bool:
+        """Whether the push counts next-cell keys per run (heavy-cell sets;
+        decided by the native plan at the first binning after a load)."""
+        return bool(_native.load().pif_push_aggregated(self.handle))
+
     def configure(self, *, q: float, m: float, externals, dt: float, shape: str = "delta"):
         """(Re)set the per-run constants: charge/mass per particle, the Boris
         constants exactly as numpy forms them (pif.py:146-153), the external
@@ -428,7 +434,8 @@ class PifEngine:
         self.allreduce()
         self.solve_fields()
 
-    def run_host(self, xh, vh, id0: int, steps: int, energy_out=None, n_chunks: int = 16):
+    def run_host(self, xh, vh, id0: int, steps: int, energy_out=None, n_chunks: int = 16,
+                 trace=None):
         """pif_step-style stepping of a host-resident ensemble (the reference's
         ParticleEnsemble use, pif.py:178-190): every step uploads x, v ((M,3),
         id order, ids id0 .. id0+M-1) from host memory, bins, deposits, reduces,
@@ -441,7 +448,9 @@ class PifEngine:
         arrays round-trip chunk by chunk on two copy streams (each chunk's
         upload for step s+1 waits for that chunk's download of step s), x
         chunks first, so both PCIe directions stay busy.  Pin xh / vh (torch
-        pin_memory) for asynchronous copies."""
+        pin_memory) for asynchronous copies.  trace: a list that receives, per
+        step, timing events (step start, x in, fields done, v in, push done,
+        downloads done, uploads done) for tools/e2e_timeline.py."""
         torch = require_cuda()
         M, dev = self.count, self.device
         if tuple(xh.shape) != (M, 3) or tuple(vh.shape) != (M, 3):
@@ -463,13 +472,24 @@ class PifEngine:
             vd.copy_(vh, non_blocking=True)
             v_in = ev()
             v_in.record(up)
+        def mark(stream):
+            if trace is None:
+                return None
+            m = torch.cuda.Event(enable_timing=True)
+            m.record(stream)
+            return m
+
         for s in range(steps):
+            t_start = mark(main)
             main.wait_event(x_in)
+            t_x = mark(main)
             self.load_aos(xd, None, id0)
             self.deposit()
             self.allreduce()
             self.solve_fields()
+            t_fields = mark(main)
             main.wait_event(v_in)
+            t_v = mark(main)
             self.load_velocities(vd)
             # the push also writes x, v in id order into the staging arrays
             _native.call("pif_set_id_order_output", self.handle, xd.data_ptr(), vd.data_ptr(),
@@ -480,6 +500,7 @@ class PifEngine:
                 _native.call("pif_set_id_order_output", self.handle, None, None, 0)
             if energy_out is not None:
                 energy_out[s:s + 1].copy_(self.scalars[0:1], non_blocking=True)
+            t_push = mark(main)
             down.wait_stream(main)
             last = s == steps - 1
             for src, dst_h, which in ((xd, xh, "x"), (vd, vh, "v")):
@@ -497,6 +518,8 @@ class PifEngine:
                         x_in = e
                     else:
                         v_in = e
+            if trace is not None:
+                trace.append((t_start, t_x, t_fields, t_v, t_push, mark(down), mark(up)))
         main.wait_stream(down)
         main.wait_stream(up)
         for t in (xd, vd):

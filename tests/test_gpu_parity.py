@@ -661,6 +661,44 @@ def test_weight_cache_matches_recomputed_weights(cuda, monkeypatch):
     assert rel_max(tables[3], tables[1]) <= 1e-12
 
 
+def test_push_count_aggregation_matches_per_particle_counts(cuda, monkeypatch):
+    """Heavy cells (Penning cloud, ~100 work items in the central segments):
+    the push's per-run next-cell counts (chosen automatically here) step
+    identically to per-particle counts, eager and from a CUDA graph; a
+    uniform set keeps per-particle counts."""
+    import torch
+
+    from paper_2605_10729_b200.engine import PifEngine
+    spec = pb.penning_spec(N=16, ppm=512, seed=2)
+    M = spec.num_particles
+    ens = pb.sample_penning(spec, 1)
+    out = []
+    for flag in ("auto", "0"):
+        if flag == "auto":
+            monkeypatch.delenv("PIF_PUSH_AGG", raising=False)
+        else:
+            monkeypatch.setenv("PIF_PUSH_AGG", flag)
+        plan = pb.make_plan(spec.N, spec.L, 1e-7)   # fresh native plan: env read at creation
+        eng = PifEngine(plan, M, "cuda", q=ens.q_per_particle, m=ens.m_per_particle,
+                        externals=spec.externals(), dt=spec.dt)
+        eng.load(ens.x, ens.v, ens.ids)
+        assert eng.push_aggregated == (flag == "auto")
+        out.append(eng.run(4, graph=False).cpu().numpy())
+        out.append(eng.run(12, graph=True).cpu().numpy())
+        x, v = eng.to_id_order()
+        out.append(torch.cat([x, v], 1).cpu().numpy())
+    for a, b in zip(out[:3], out[3:]):
+        assert rel_max(a, b) <= 1e-12
+    monkeypatch.delenv("PIF_PUSH_AGG", raising=False)
+    lspec = pb.landau_spec(N=16, ppm=64, seed=1)
+    plan = pb.make_plan(lspec.N, lspec.L, 1e-7)
+    eng = PifEngine(plan, lspec.num_particles, "cuda", q=-1.0, m=1.0,
+                    externals=lspec.externals(), dt=lspec.dt)
+    lens = pb.sample_landau(lspec, 1)
+    eng.load(lens.x, lens.v, lens.ids)
+    assert not eng.push_aggregated
+
+
 def test_pd_run_with_device_sampler_matches_reference_trace():
     """RunSetup(sampler="device"): ranks regenerate their slices of the reference
     ensemble in HBM; the 20-step trace still matches the reference's PD-2 trace."""
