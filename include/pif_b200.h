@@ -37,6 +37,9 @@ extern "C" {
 #define PIF_SHAPE_CIC 1       /* pif.py:79-85 */
 #define PIF_EXT_NONE 0        /* pif.py:50-51 */
 #define PIF_EXT_QUADRUPOLE 1  /* pif.py:52-57 */
+#define PIF_PERMUTE_POSITIONS 1   /* pif_permute: x, y, z, id           */
+#define PIF_PERMUTE_VELOCITIES 2  /* pif_permute: vx, vy, vz              */
+#define PIF_PERMUTE_RESET 4       /* pif_permute: then perm[i] = i        */
 
 typedef struct pif_plan_s *pif_plan_t;
 
@@ -211,9 +214,19 @@ int pif_load_aos(pif_plan_t plan, const double *x, const double *v, int64_t id0,
 /* pif_load_aos with v == NULL loads positions (and keys) only, so binning and
  * the deposit can start while the velocities are still on the way;
  * pif_load_aos_velocities then fills dst's velocities from the (M,3) rows
- * (same set, before any push).  rank may be NULL (pif_bin_perm with NULL
- * rank assigns the in-cell slots). */
+ * (same set, before any push): slot i takes row dst->id[i] - id0, so it also
+ * works after pif_permute.  rank may be NULL (pif_bin_perm with NULL rank
+ * assigns the in-cell slots). */
 int pif_load_aos_velocities(pif_plan_t plan, const double *v, pif_soa_t *dst, void *stream);
+/* dst[i] = src[perm[i]] for the fields `what` selects (PIF_PERMUTE_*), i <
+ * src->count; PIF_PERMUTE_RESET afterwards sets perm to the identity.  No
+ * reference counterpart (its particles are never reordered): the data
+ * movement step of a host-streamed step (PifEngine.run_host), where the set
+ * arrives in id order (spatially random) and is put into the cell order of
+ * pif_bin_perm once, so the spread and the gather read it coalesced.  dst
+ * must not alias src. */
+int pif_permute(pif_plan_t plan, const pif_soa_t *src, int32_t *perm, pif_soa_t *dst, int what,
+                void *stream);
 int pif_set_id_order_output(pif_plan_t plan, double *x_out, double *v_out, int64_t id0);
 /* Diagnostic sums of a particle set (Recorder.record, strategies.py:96-106). */
 int pif_particle_diag(pif_plan_t plan, const pif_soa_t *p, int e_kind, double *diag,

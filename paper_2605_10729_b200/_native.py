@@ -15,6 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PIF_B200_LIB", os.path.join(_HERE, "libpifb200.so"))
 
 PIF_OK, PIF_ERR_VALUE, PIF_ERR_CUDA, PIF_ERR_STATE = 0, 1, 2, 3
+PIF_PERMUTE_POSITIONS, PIF_PERMUTE_VELOCITIES, PIF_PERMUTE_RESET = 1, 2, 4
 SHAPE = {"delta": 0, "cic": 1}
 EXT = {"none": 0, "quadrupole": 1}
 
@@ -85,6 +86,7 @@ SIGNATURES = {
     "pif_set_deterministic": ([_P, _I], _I),
     "pif_is_deterministic": ([_P], _I),
     "pif_push_aggregated": ([_P], _I),
+    "pif_permute": ([_P, _SOA, _P, _SOA, _I, _P], _I),
     "pif_nccl_version": ([ctypes.POINTER(ctypes.c_int)], _I),
     "pif_comm_init_all": ([_I, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_P)], _I),
     "pif_allreduce_f64": ([_P, _P, _I64, _P], _I),
@@ -106,7 +108,12 @@ def load():
                     f"{LIB_PATH} is missing: build the CUDA extension first "
                     "(python -m paper_2605_10729_b200.build); there is no CPU fallback")
             lib = ctypes.CDLL(LIB_PATH)
+            # an A/B build named by PIF_B200_LIB may predate newer entry
+            # points; the in-tree library must export all of them
+            ab = "PIF_B200_LIB" in os.environ
             for name, (args, res) in SIGNATURES.items():
+                if ab and not hasattr(lib, name):
+                    continue
                 fn = getattr(lib, name)
                 fn.argtypes = args
                 fn.restype = res

@@ -576,6 +576,25 @@ int pif_load_aos(pif_plan_t plan, const double *x, const double *v, int64_t id0,
     return pif::launch_load_aos(p, x, v, id0, *dst, key, rank, s);
 }
 
+int pif_permute(pif_plan_t plan, const pif_soa_t *src, int32_t *perm, pif_soa_t *dst, int what,
+                void *stream) {
+    PLAN_CHECK();
+    if (!src || !dst) return pif::bad("invalid particle view");
+    const int all = PIF_PERMUTE_POSITIONS | PIF_PERMUTE_VELOCITIES | PIF_PERMUTE_RESET;
+    if (what & ~all) return pif::bad("unknown permute flags");
+    const bool vel = (what & PIF_PERMUTE_VELOCITIES) != 0;
+    if (!pif::soa_ok(src, vel)) return pif::bad("invalid source view");
+    pif_soa_t d = *dst;
+    d.count = src->count;
+    if (!pif::soa_ok(&d, vel)) return pif::bad("invalid destination view");
+    if (d.count > 0 && !perm) return pif::bad("missing perm");
+    if ((what & PIF_PERMUTE_POSITIONS) && d.x == src->x) return pif::bad("dst must not alias src");
+    if (vel && d.vx == src->vx) return pif::bad("dst must not alias src");
+    const int rc = pif::launch_permute(p, *src, perm, d, what, s);
+    dst->count = d.count;
+    return rc;
+}
+
 int pif_load_aos_velocities(pif_plan_t plan, const double *v, pif_soa_t *dst, void *stream) {
     PLAN_CHECK();
     if (!pif::soa_ok(dst, true)) return pif::bad("invalid destination view");

@@ -133,12 +133,17 @@ __global__ void load_aos_kernel(const double *__restrict__ xa, const double *__r
 
 // the velocities of a set loaded with load_aos_kernel(va = NULL): AoS rows of
 // ids id0 .. id0+M-1 -> SoA slots i (the load left particle i in slot i)
-__global__ void load_vel_kernel(const double *__restrict__ va, int64_t M, pif_soa_t dst) {
+// slot i takes the row of its own id (i itself right after the load; any
+// slot after pif_permute)
+__global__ void load_vel_kernel(const double *__restrict__ va, int64_t id0, int64_t M,
+                                pif_soa_t dst) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < M;
          i += (int64_t)gridDim.x * blockDim.x) {
-        dst.vx[i] = va[3 * i];
-        dst.vy[i] = va[3 * i + 1];
-        dst.vz[i] = va[3 * i + 2];
+        const int64_t r = dst.id[i] - id0;
+        PIF_CHECK(r >= 0 && r < M);
+        dst.vx[i] = va[3 * r];
+        dst.vy[i] = va[3 * r + 1];
+        dst.vz[i] = va[3 * r + 2];
     }
 }
 
@@ -233,6 +238,12 @@ __device__ __forceinline__ void dmma884(double &d0, double &d1, double a, double
 // never written) and laid out so the DMMA fragment loads are conflict-free or
 // 2-way (row strides 33 and 9 doubles).
 constexpr int kChunk = 32;
+// accumulator chains per gather sub-batch: 3 (one per component; default,
+// gather 17.38 -> 17.17 ms at 2^27) or 6 (per half-slot and component, merged
+// by 6 DADDs per sub-batch)
+#ifndef PIF_GATHER_CHAINS
+#define PIF_GATHER_CHAINS 3
+#endif
 
 // Layouts chosen so the hot shared-memory accesses are bank-conflict free
 // (64-bit words, 16 per half-warp phase): wz is [c][p] with row stride 36
@@ -711,6 +722,27 @@ __device__ __forceinline__ void gather_sub_d(WarpChunk &st, GatherPartials &gp,
         A[a][0] = wxa * bz0;
         A[a][1] = wxa * bz1;
     }
+#if PIF_GATHER_CHAINS == 3
+    // one accumulator chain per component (16 DMMAs each, interleaved: a
+    // chain's next DMMA issues 3 DMMAs = 48 clk later, past the ~29 clk DMMA
+    // latency), so no per-sub-batch merge adds
+    double D[3][2];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) D[d][0] = D[d][1] = 0.0;
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) dmma884(D[d][0], D[d][1], A[a][hh], g[a][hh][d]);
+    if (r < m) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            gp.D[d][2 * c4][j + r] = D[d][0];
+            gp.D[d][2 * c4 + 1][j + r] = D[d][1];
+        }
+    }
+#else
     double Dh[2][3][2];
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh)
@@ -730,6 +762,7 @@ __device__ __forceinline__ void gather_sub_d(WarpChunk &st, GatherPartials &gp,
             gp.D[d][2 * c4 + 1][j + r] = Dh[0][d][1] + Dh[1][d][1];
         }
     }
+#endif
 }
 
 // A sub-batch of m < 8 particles without the tensor cores: lane (r, c4) adds
@@ -1704,11 +1737,12 @@ int ensure_ring_scratch(Plan &p, int64_t M) {
     return PIF_OK;
 }
 
-// Density thresholds of the ring kernels (Plan::ring_spread_min = 0,
+// Density thresholds of the ring kernels (Plan::ring_spread_min = 0.1,
 // ring_gather_min = 0.75 particles per stencil cell).  With segments of up to
 // 127 cells and zero planes skipped, the ring spreader beats the
-// one-thread-per-particle atomics at every density measured (0.125 per cell:
-// 2.3x / 1.9x at w = 13 / 10); the ring gather, which reloads a plane per cell
+// one-thread-per-particle atomics down to ~0.1 per cell (0.125 per cell:
+// 2.3x / 1.9x at w = 13 / 10; at 0.06 and 0.008 per cell walking the empty
+// cells makes it 2.4x / 3.1x slower); the ring gather, which reloads a plane per cell
 // step, wins from ~1 per cell (1.5x / 2.5x) and loses below (0.5 per cell:
 // -6% / -45% at w = 13 / 16; 0.125: -90% / -40% at w = 13 / 10).
 // profiles/round2/ring_density_ab.txt
@@ -1866,6 +1900,41 @@ int build_items(Plan &p, int64_t M, cudaStream_t s) {
     return PIF_OK;
 }
 
+// dst[slot] = src[perm[slot]] (what: PIF_PERMUTE_POSITIONS x, y, z, id;
+// PIF_PERMUTE_VELOCITIES vx, vy, vz; PIF_PERMUTE_RESET then perm[slot] = slot).
+// A set loaded in id order from host memory is spatially random, and the
+// kernels reading it through perm would gather 8-byte words at random with
+// few warps in flight; one streaming pass with full occupancy puts it in
+// cell order instead (random reads, coalesced writes).
+__global__ void permute_kernel(pif_soa_t src, int32_t *__restrict__ perm, pif_soa_t dst, int what) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < dst.count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t j = perm[i];
+        if (what & PIF_PERMUTE_POSITIONS) {
+            const double x = src.x[j], y = src.y[j], z = src.z[j];
+            const int64_t id = src.id[j];
+            dst.x[i] = x;
+            dst.y[i] = y;
+            dst.z[i] = z;
+            dst.id[i] = id;
+        }
+        if (what & PIF_PERMUTE_VELOCITIES) {
+            const double vx = src.vx[j], vy = src.vy[j], vz = src.vz[j];
+            dst.vx[i] = vx;
+            dst.vy[i] = vy;
+            dst.vz[i] = vz;
+        }
+        if (what & PIF_PERMUTE_RESET) perm[i] = (int32_t)i;
+    }
+}
+
+int launch_permute(Plan &p, const pif_soa_t &src, int32_t *perm, pif_soa_t &dst, int what,
+                   cudaStream_t s) {
+    if (dst.count == 0) return PIF_OK;
+    permute_kernel<<<grid_for(dst.count, 256, p.sm_count), 256, 0, s>>>(src, perm, dst, what);
+    return fail_cuda(cudaGetLastError(), "permute_kernel");
+}
+
 int launch_soa_to_aos(Plan &p, const pif_soa_t &P, int64_t id0, double *ox, double *ov,
                       cudaStream_t s) {
     if (P.count == 0) return PIF_OK;
@@ -1890,13 +1959,15 @@ int debug_phase_cycles(unsigned long long *out) {
 
 int launch_load_velocities(Plan &p, const double *v, pif_soa_t &dst, cudaStream_t s) {
     if (dst.count == 0) return PIF_OK;
-    load_vel_kernel<<<grid_for(dst.count, 256, p.sm_count), 256, 0, s>>>(v, dst.count, dst);
+    load_vel_kernel<<<grid_for(dst.count, 256, p.sm_count), 256, 0, s>>>(v, p.aos_id0, dst.count,
+                                                                        dst);
     return fail_cuda(cudaGetLastError(), "load_vel_kernel");
 }
 
 int launch_load_aos(Plan &p, const double *x, const double *v, int64_t id0, pif_soa_t &dst,
                     int32_t *key, int32_t *rank, cudaStream_t s) {
     p.wcache_valid = false;
+    p.aos_id0 = id0;
     if (dst.count == 0) return PIF_OK;
     load_aos_kernel<<<grid_for(dst.count, 256, p.sm_count), 256, 0, s>>>(
         x, v, id0, dst.count, dst, p.L, p.h, p.w, p.n, key, rank, p.cell_count);

@@ -50,7 +50,7 @@ struct Plan {
     int64_t n3 = 0, nhalf = 0;     // n^3, n*n*(n/2+1)
     int seg = 8;                   // cells per z-segment work item (set per binning)
     int seg_target = 1024;         // particles per work item the segment length aims at
-    double ring_spread_min = 0.0;   // ring kernels from this many particles per stencil cell
+    double ring_spread_min = 0.1;   // ring kernels from this many particles per stencil cell
     double ring_gather_min = 0.75;  // (PIF_RING_SPREAD_MIN / PIF_RING_GATHER_MIN override, A/B)
     double density = 0.0;          // particles per stencil cell at the last binning
     double *ring_scratch = nullptr;  // E per position for the wide-window gather
@@ -91,6 +91,7 @@ struct Plan {
     // segment at the first binning after a load (agg_check; never inside a
     // graph capture); PIF_PUSH_AGG=0/1 forces it.
     bool push_agg = false;
+    int64_t aos_id0 = 0;           // id of row 0 of the last pif_load_aos (velocities by id)
     bool agg_check = true;
     int push_agg_force = -1;
     int n_segs = 0;
@@ -151,6 +152,8 @@ int launch_type2_complex_sorted(Plan &p, const double *modes, const pif_soa_t &s
 int launch_load_aos(Plan &p, const double *x, const double *v, int64_t id0, pif_soa_t &dst,
                     int32_t *key, int32_t *rank, cudaStream_t s);
 int launch_load_velocities(Plan &p, const double *v, pif_soa_t &dst, cudaStream_t s);
+int launch_permute(Plan &p, const pif_soa_t &src, int32_t *perm, pif_soa_t &dst, int what,
+                   cudaStream_t s);
 int launch_interp(Plan &p, const pif_soa_t &src, const int32_t *perm, pif_soa_t &dst, bool push,
                   double half, double dt, const double *tq, const double *sq, int has_b,
                   int e_kind, int32_t *key, int32_t *rank, double *diag, double *E_out,

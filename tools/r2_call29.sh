@@ -23,3 +23,10 @@ echo done
 timeout 600 python tools/e2e_timeline.py 27 16 > gpurun_out/c29_e2e_timeline.txt 2>&1
 timeout 300 python tools/pcie_probe.py > gpurun_out/c29_pcie.txt 2>&1
 echo done2
+for rep in 1 2; do
+  for lib in lib_chains6 lib_chains3; do
+    PIF_B200_LIB=$L/$lib.so timeout 600 python bench.py --steps 10 --warmup 3 --no-e2e \
+      --no-cpu-baseline > gpurun_out/c29_landau_${lib}_$rep.json 2> /dev/null
+  done
+done
+echo done3
