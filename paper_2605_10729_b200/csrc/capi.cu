@@ -58,6 +58,7 @@ void release(Plan &p) {
                     p.dbuf, p.det_keys, p.det_iota, p.det_tmp};
     for (void *q : ptrs)
         if (q) cudaFree(q);
+    if (p.max_parts_host) cudaFreeHost(p.max_parts_host);
     if (p.d2z) cufftDestroy(p.d2z);
     if (p.z2d3) cufftDestroy(p.z2d3);
     if (p.fft_ev) {

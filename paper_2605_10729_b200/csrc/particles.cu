@@ -209,6 +209,8 @@ __global__ void seg_items_kernel(const int *__restrict__ parts, const int *__res
     }
 }
 
+__global__ void publish_int_kernel(const int *__restrict__ src, volatile int *dst) { *dst = *src; }
+
 __global__ void max_parts_kernel(const int *__restrict__ parts, int nsegs, int *out) {
     int m = 0;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nsegs; i += gridDim.x * blockDim.x)
@@ -1884,16 +1886,27 @@ int build_items(Plan &p, int64_t M, cudaStream_t s) {
         e = cudaStreamIsCapturing(s, &cs);
         if (e != cudaSuccess) return fail_cuda(e, "capture status");
         if (cs == cudaStreamCaptureStatusNone) {
-            int mp = 0;
-            e = cudaMemsetAsync(p.max_parts, 0, sizeof(int), s);
+            // the value reaches the host through mapped pinned memory (a
+            // kernel store), not a D2H copy: a copy would queue behind
+            // whatever the copy engine is streaming (run_host: the previous
+            // step's velocities, ~55 ms)
+            if (!p.max_parts_host) {
+                e = cudaHostAlloc(reinterpret_cast<void **>(&p.max_parts_host), sizeof(int),
+                                  cudaHostAllocMapped);
+                if (e != cudaSuccess) return fail_cuda(e, "mapped host word");
+            }
+            int *mapped = nullptr;
+            e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&mapped), p.max_parts_host, 0);
+            if (e == cudaSuccess) e = cudaMemsetAsync(p.max_parts, 0, sizeof(int), s);
             if (e == cudaSuccess) {
                 max_parts_kernel<<<grid_for(p.n_segs, 256, p.sm_count), 256, 0, s>>>(
                     p.seg_parts, p.n_segs, p.max_parts);
-                e = cudaMemcpyAsync(&mp, p.max_parts, sizeof(int), cudaMemcpyDeviceToHost, s);
+                publish_int_kernel<<<1, 1, 0, s>>>(p.max_parts, mapped);
+                e = cudaGetLastError();
             }
             if (e == cudaSuccess) e = cudaStreamSynchronize(s);
             if (e != cudaSuccess) return fail_cuda(e, "max parts per segment");
-            p.push_agg = mp >= kPushAggMinParts;
+            p.push_agg = *reinterpret_cast<volatile int *>(p.max_parts_host) >= kPushAggMinParts;
             p.agg_check = false;
         }
     }

@@ -85,6 +85,7 @@ struct Plan {
     int *seg_parts = nullptr;      // n_segs + 1
     int *seg_off = nullptr;        // n_segs + 1; seg_off[n_segs] = number of items
     int *max_parts = nullptr;      // (1) most parts in one segment (push_agg decision)
+    int *max_parts_host = nullptr; // mapped pinned copy of it
     // push_agg: the gather+push kernel counts next-cell keys per run of equal
     // keys in dense segments instead of per particle (heavy cells: per-lane
     // REDs to one counter serialise in L2).  Decided from the parts per

@@ -23,6 +23,7 @@ The records come back to the host once, at the end of the run.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -453,6 +454,7 @@ class PifEngine:
         downloads done, uploads done) for tools/e2e_timeline.py."""
         torch = require_cuda()
         M, dev = self.count, self.device
+        scatter_after = os.environ.get("PIF_E2E_SCATTER", "0") == "1"
         if tuple(xh.shape) != (M, 3) or tuple(vh.shape) != (M, 3):
             raise ValueError(f"host arrays must be ({M}, 3)")
         main = torch.cuda.current_stream(dev)
@@ -484,21 +486,30 @@ class PifEngine:
             main.wait_event(x_in)
             t_x = mark(main)
             self.load_aos(xd, None, id0)
+            t_bin = mark(main)
             self._to_cell_order(_native.PIF_PERMUTE_POSITIONS)
+            t_perm = mark(main)
             self.deposit()
+            t_dep = mark(main)
             self.allreduce()
             self.solve_fields()
             t_fields = mark(main)
             main.wait_event(v_in)
             t_v = mark(main)
             self.load_velocities(vd)
-            # the push also writes x, v in id order into the staging arrays
-            _native.call("pif_set_id_order_output", self.handle, xd.data_ptr(), vd.data_ptr(),
-                         int(id0))
-            try:
-                self.gather_push()
-            finally:
-                _native.call("pif_set_id_order_output", self.handle, None, None, 0)
+            if scatter_after:
+                # push, then one streaming scatter of the pushed set to id order
+                self.interp_push()
+                self.to_id_order(xd, vd, id0)
+                self.rebin()
+            else:
+                # the push also writes x, v in id order into the staging arrays
+                _native.call("pif_set_id_order_output", self.handle, xd.data_ptr(),
+                             vd.data_ptr(), int(id0))
+                try:
+                    self.gather_push()
+                finally:
+                    _native.call("pif_set_id_order_output", self.handle, None, None, 0)
             if energy_out is not None:
                 energy_out[s:s + 1].copy_(self.scalars[0:1], non_blocking=True)
             t_push = mark(main)
@@ -520,7 +531,8 @@ class PifEngine:
                     else:
                         v_in = e
             if trace is not None:
-                trace.append((t_start, t_x, t_fields, t_v, t_push, mark(down), mark(up)))
+                trace.append((t_start, t_x, t_fields, t_v, t_push, mark(down), mark(up), t_bin,
+                              t_perm, t_dep))
         main.wait_stream(down)
         main.wait_stream(up)
         for t in (xd, vd):

@@ -38,10 +38,13 @@ print(f"M = 2^{lm}, {chunks} chunks; ms from the first step's start")
 names = ("start", "x in", "fields", "v in", "push", "D2H end", "H2D end")
 print("step " + "".join(f"{n:>10}" for n in names))
 for s, evs in enumerate(tr):
-    print(f"{s:4d} " + "".join(f"{t0.elapsed_time(e):10.1f}" for e in evs))
-prev = None
+    print(f"{s:4d} " + "".join(f"{t0.elapsed_time(e):10.1f}" for e in evs[:7]))
 for s, evs in enumerate(tr):
-    st, xi, fi, vi, pu, dn, upd = evs
+    st, xi, fi, vi, pu, dn, upd, tb, tp, td = evs
+    print(f"step {s}: load_aos+bin {xi.elapsed_time(tb):.1f}, permute {tb.elapsed_time(tp):.1f},"
+          f" deposit {tp.elapsed_time(td):.1f}, allreduce+solve {td.elapsed_time(fi):.1f}")
+for s, evs in enumerate(tr):
+    st, xi, fi, vi, pu, dn, upd = evs[:7]
     print(f"step {s}: wait x {st.elapsed_time(xi):.1f}, load+bin+deposit+solve {xi.elapsed_time(fi):.1f},"
           f" wait v {fi.elapsed_time(vi):.1f}, v load+gather+push {vi.elapsed_time(pu):.1f},"
           f" push->D2H end {pu.elapsed_time(dn):.1f}, push->H2D end {pu.elapsed_time(upd):.1f}")
