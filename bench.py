@@ -455,6 +455,13 @@ def run_e2e(a, eng, torch, dist, world, per_gpu, glob, dev):
     e.record()
     torch.cuda.synchronize(dev)
     T = s.elapsed_time(e) * 1e-3
+    if os.environ.get("PIF_E2E_TRACE") == "1":   # per-step marks to stderr (diagnosis)
+        tr = []
+        eng.run_host(xh, vh, lo, 4, energy_out=wh, trace=tr)
+        torch.cuda.synchronize(dev)
+        for i, evs in enumerate(tr):
+            print("e2e trace step", i, " ".join(f"{evs[0].elapsed_time(x):.1f}" for x in evs[:7]),
+                  file=sys.stderr)
     if world > 1:
         tt = torch.tensor([T], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)

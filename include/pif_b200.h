@@ -165,6 +165,26 @@ int pif_interp_push_perm(pif_plan_t plan, const pif_soa_t *src, const int32_t *p
                          pif_soa_t *dst, double half, double dt, const double tq[3],
                          const double sq[3], int has_b, int e_kind, int32_t *key, int32_t *rank,
                          double *diag, void *stream);
+/* The same step in two parts, for host-streamed stepping (the gather only
+ * needs positions; the push needs the velocities, which may still be on the
+ * way from the host):
+ * pif_interp_split: gather E (interp_r3, _kernels.py:125-183) at every
+ *   particle of src (read through perm) into a plan-owned (M,3) array, row
+ *   id - id0 (src holds ids id0 .. id0+M-1);
+ * pif_push_ids: Boris push (pif.py:140-158; E_ext pif.py:43-57; wrap
+ *   particles.py:65-70) of rows [row0, row0+rows) of device (M,3) x, v in id
+ *   order (the host ParticleEnsemble layout) in place with those E rows.
+ *   Chunks may be pushed in any number of calls in increasing row order; the
+ *   call that reaches row M writes diag ({sum v.v, sum vx, sum vy, sum vz,
+ *   sum phi_ext, 0}, like pif_interp_push_perm).  No cell keys are written:
+ *   the caller rebins from the pushed rows (pif_load_aos).
+ * DMMA kernels only (w <= 8): pif_split_supported returns 1 / 0. */
+int pif_interp_split(pif_plan_t plan, const pif_soa_t *src, const int32_t *perm, int64_t id0,
+                     void *stream);
+int pif_push_ids(pif_plan_t plan, double *x, double *v, int64_t M, int64_t row0, int64_t rows,
+                 double half, double dt, const double tq[3], const double sq[3], int has_b,
+                 int e_kind, double *diag, void *stream);
+int pif_split_supported(pif_plan_t plan);
 /* Gather only (gather_efield): E at the sorted particles written to
  * E_out[3*id + d] (AoS, particle id order). */
 int pif_interp_sorted(pif_plan_t plan, const pif_soa_t *sorted, double *E_out, void *stream);

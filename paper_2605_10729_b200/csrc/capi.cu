@@ -401,6 +401,32 @@ int pif_interp_push_perm(pif_plan_t plan, const pif_soa_t *src, const int32_t *p
     return rc;
 }
 
+int pif_interp_split(pif_plan_t plan, const pif_soa_t *src, const int32_t *perm, int64_t id0,
+                     void *stream) {
+    PLAN_CHECK();
+    if (!pif::soa_ok(src, false)) return pif::bad("invalid particle view");
+    if (src->count > 0 && !perm) return pif::bad("missing perm");
+    return pif::launch_interp_split(p, *src, perm, id0, s);
+}
+
+int pif_push_ids(pif_plan_t plan, double *x, double *v, int64_t M, int64_t row0, int64_t rows,
+                 double half, double dt, const double tq[3], const double sq[3], int has_b,
+                 int e_kind, double *diag, void *stream) {
+    PLAN_CHECK();
+    if (M < 0 || row0 < 0 || rows < 0 || row0 + rows > M) return pif::bad("invalid row range");
+    if (M > 0 && (!x || !v)) return pif::bad("null x/v rows");
+    if (!diag) return pif::bad("null diag");
+    if (e_kind != PIF_EXT_NONE && e_kind != PIF_EXT_QUADRUPOLE) return pif::bad("unknown e_kind");
+    if (!(dt > 0)) return pif::bad("dt must be positive");
+    return pif::launch_push_ids(p, x, v, M, row0, row0 + rows, half, dt, tq, sq, has_b, e_kind,
+                                diag, s);
+}
+
+int pif_split_supported(pif_plan_t plan) {
+    if (!plan) return pif::bad("null plan");
+    return pif::split_supported(plan->p) ? 1 : 0;
+}
+
 
 int pif_set_deterministic(pif_plan_t plan, int enable) {
     if (!plan) return pif::bad("null plan");

@@ -608,6 +608,7 @@ struct PushParams {
     int has_b, e_kind, n, w;
     double *mx, *mv;      // id-order mirror (pif_set_id_order_output) or null
     long long mid0;
+    double *eslot;        // gather only: E rows id - mid0 of an (M,3) array (pif_interp_split)
 };
 
 // pushed particle also written to row id - mid0 of the (M,3) mirrors
@@ -1092,6 +1093,11 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                         if (agg) ckey = kk;
                         else atomicAdd(&count[kk], 1);
                     }
+                } else if (pp.eslot) {   // row id - mid0, for pif_push_ids
+                    const int64_t o = 3 * (id0 - pp.mid0);
+                    pp.eslot[o] = E0;
+                    pp.eslot[o + 1] = E1;
+                    pp.eslot[o + 2] = E2;
                 } else {
                     const int64_t o = 3 * id0;
                     E_out[o] = E0;
@@ -1528,6 +1534,32 @@ __global__ void ring_push_kernel(pif_soa_t P, const int32_t *__restrict__ perm, 
     if (PUSH) block_diag_store(dg, partials);
 }
 
+// Boris push of id-ordered (M,3) host-layout rows in place, with the E rows a
+// split gather wrote (pif_interp_split): the push phase of
+// interp_mma_kernel<PUSH> (same boris_one, same wrap of the loaded positions
+// as load_aos_kernel) as a coalesced streaming pass over rows [r0, r1), for
+// host-streamed stepping (PifEngine.run_host): the next step rebins from the
+// downloaded rows, so no cell keys, counts or SoA copy are written, and each
+// chunk of rows can be downloaded as soon as its launch ends.
+__global__ void __launch_bounds__(256)
+push_ids_kernel(double *__restrict__ xa, double *__restrict__ va,
+                const double *__restrict__ Ea, int64_t r0, int64_t r1, PushParams pp,
+                double *__restrict__ partials) {
+    double dg[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    const double L = pp.L;
+    for (int64_t r = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < r1;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t o = 3 * r;
+        double x = wrap_coord(xa[o], L), y = wrap_coord(xa[o + 1], L),
+               z = wrap_coord(xa[o + 2], L);
+        double vx = va[o], vy = va[o + 1], vz = va[o + 2];
+        boris_one(pp, Ea[o], Ea[o + 1], Ea[o + 2], x, y, z, vx, vy, vz, dg);
+        xa[o] = x; xa[o + 1] = y; xa[o + 2] = z;
+        va[o] = vx; va[o + 1] = vy; va[o + 2] = vz;
+    }
+    block_diag_store(dg, partials);
+}
+
 // ----------------------------------------------------------------------------
 // generic one-thread-per-particle kernels (any w <= kMaxW)
 // ----------------------------------------------------------------------------
@@ -1789,6 +1821,7 @@ PushParams make_push(const Plan &p, double half, double dt, const double *tq, co
     pp.mx = p.mirror_x;
     pp.mv = p.mirror_v;
     pp.mid0 = p.mirror_id0;
+    pp.eslot = nullptr;
     return pp;
 }
 
@@ -2187,15 +2220,18 @@ int ensure_wcache(Plan &p, int64_t M) {
     return PIF_OK;
 }
 
-int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q, bool push,
-                  double half, double dt, const double *tq, const double *sq, int has_b,
-                  int e_kind, int32_t *key, int32_t *rank, double *diag, double *E_out,
-                  cudaStream_t s) {
+namespace {
+int interp_impl(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q, bool push,
+                double half, double dt, const double *tq, const double *sq, int has_b,
+                int e_kind, int32_t *key, int32_t *rank, double *diag, double *E_out,
+                double *eslot, int64_t eslot_id0, cudaStream_t s) {
     if (!p.field_valid) {
         set_error("no field grid: solve the fields before gathering");
         return PIF_ERR_STATE;
     }
     PushParams pp = make_push(p, half, dt, tq, sq, has_b, e_kind);
+    pp.eslot = eslot;
+    if (eslot) pp.mid0 = eslot_id0;
     const EsPoly poly = device_poly(p);
     const double4 *field = reinterpret_cast<const double4 *>(p.field);
     cudaError_t e;
@@ -2258,6 +2294,9 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
                 return PIF_ERR_VALUE;
         }
 #undef PIF_INTERP_CASE
+    } else if (eslot && P.count > 0) {
+        set_error("split gather: DMMA kernels (w <= 8) only");
+        return PIF_ERR_STATE;
     } else if (P.count > 0 && ring_path_ok(p) && p.density >= p.ring_gather_min) {
         const int nseg = (p.n + p.seg - 1) / p.seg;
         const int *nitems = p.seg_off + p.n_segs;
@@ -2324,6 +2363,74 @@ int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q
         return fail_cuda(cudaGetLastError(), "finish_diag_kernel");
     }
     return PIF_OK;
+}
+}  // namespace
+
+int launch_interp(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q, bool push,
+                  double half, double dt, const double *tq, const double *sq, int has_b,
+                  int e_kind, int32_t *key, int32_t *rank, double *diag, double *E_out,
+                  cudaStream_t s) {
+    p.split_valid = false;
+    return interp_impl(p, P, perm, Q, push, half, dt, tq, sq, has_b, e_kind, key, rank, diag,
+                       E_out, nullptr, 0, s);
+}
+
+bool split_supported(const Plan &p) { return fast_path_ok(p); }
+
+int launch_interp_split(Plan &p, const pif_soa_t &P, const int32_t *perm, int64_t id0,
+                        cudaStream_t s) {
+    p.split_valid = false;
+    if (!split_supported(p)) {
+        set_error("split gather: DMMA kernels (w <= 8) only");
+        return PIF_ERR_STATE;
+    }
+    if (ensure_ring_scratch(p, P.count) != PIF_OK) return PIF_ERR_CUDA;
+    pif_soa_t Q = P;
+    const int rc = interp_impl(p, P, perm, Q, false, 0.0, 1.0, nullptr, nullptr, 0, PIF_EXT_NONE,
+                               nullptr, nullptr, nullptr, nullptr, p.ring_scratch, id0, s);
+    if (rc == PIF_OK) {
+        p.split_valid = true;
+        p.split_count = P.count;
+        p.split_parts = 0;
+    }
+    return rc;
+}
+
+int launch_push_ids(Plan &p, double *x, double *v, int64_t M, int64_t r0, int64_t r1,
+                    double half, double dt, const double *tq, const double *sq, int has_b,
+                    int e_kind, double *diag, cudaStream_t s) {
+    if (!p.split_valid || p.split_count != M) {
+        set_error("pif_push_ids: no split gather of these particles (pif_interp_split first)");
+        return PIF_ERR_STATE;
+    }
+    if (r0 == 0) p.split_parts = 0;
+    p.wcache_valid = false;   // the particles move
+    PushParams pp = make_push(p, half, dt, tq, sq, has_b, e_kind);
+    // the chunk's share of the diagnostic partial slots (rows / M of them)
+    int blocks = grid_for(r1 - r0, 256, p.sm_count);
+    const int share = (int)(((int64_t)p.partial_blocks * (r1 - r0)) / (M > 0 ? M : 1));
+    if (blocks > share) blocks = share > 0 ? share : 1;
+    const int room = p.partial_blocks - p.split_parts;
+    if (blocks > room) blocks = room;
+    if (blocks < 1) {
+        set_error("pif_push_ids: too many row chunks for the diagnostic partials");
+        return PIF_ERR_VALUE;
+    }
+    if (r1 > r0) {
+        push_ids_kernel<<<blocks, 256, 0, s>>>(x, v, p.ring_scratch, r0, r1, pp,
+                                               p.partials + (size_t)p.split_parts * kDiagSlots);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return fail_cuda(e, "push_ids_kernel");
+        p.split_parts += blocks;
+    }
+    if (r1 < M) return PIF_OK;
+    p.split_valid = false;   // every row pushed
+    if (p.split_parts == 0) {
+        const cudaError_t e = cudaMemsetAsync(diag, 0, sizeof(double) * kDiagSlots, s);
+        return fail_cuda(e, "zero diag");
+    }
+    finish_diag_kernel<<<1, 32 * kDiagSlots, 0, s>>>(p.partials, p.split_parts, diag);
+    return fail_cuda(cudaGetLastError(), "finish_diag_kernel");
 }
 
 int launch_particle_diag(Plan &p, const pif_soa_t &P, int e_kind, double *diag, cudaStream_t s) {

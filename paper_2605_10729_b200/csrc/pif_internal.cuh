@@ -65,6 +65,12 @@ struct Plan {
     double *mirror_x = nullptr;    // id-order (M,3) mirrors written by the push kernels
     double *mirror_v = nullptr;
     long long mirror_id0 = 0;
+    // split step (pif_interp_split / pif_push_ids): E rows in id order in
+    // ring_scratch, valid for split_count rows; split_parts diagnostic
+    // partial blocks used by the row chunks pushed so far
+    bool split_valid = false;
+    int64_t split_count = 0;
+    int split_parts = 0;
     double *deconv = nullptr;      // (N,)
     double *kvec = nullptr;        // (N,) 2 pi m / L
     double *grid = nullptr;        // n^3 real fine grid
@@ -159,6 +165,12 @@ int launch_interp(Plan &p, const pif_soa_t &src, const int32_t *perm, pif_soa_t 
                   double half, double dt, const double *tq, const double *sq, int has_b,
                   int e_kind, int32_t *key, int32_t *rank, double *diag, double *E_out,
                   cudaStream_t s);
+int launch_interp_split(Plan &p, const pif_soa_t &src, const int32_t *perm, int64_t id0,
+                        cudaStream_t s);
+int launch_push_ids(Plan &p, double *x, double *v, int64_t M, int64_t r0, int64_t r1,
+                    double half, double dt, const double *tq, const double *sq, int has_b,
+                    int e_kind, double *diag, cudaStream_t s);
+bool split_supported(const Plan &p);
 int launch_particle_diag(Plan &p, const pif_soa_t &ps, int e_kind, double *diag, cudaStream_t s);
 int launch_modes_from_spec(Plan &p, double *modes, cudaStream_t s);
 int launch_solve_fields(Plan &p, const double *raw, int shape, double *rho_out, double *scalars,

@@ -318,6 +318,28 @@ class PifEngine:
         if self.deterministic:      # the fused sums depend on the work-item schedule
             self.particle_diag()
 
+    def split_supported(self) -> bool:
+        """pif_interp_split / pif_push_split cover the DMMA kernels (w <= 8)."""
+        return bool(_native.load().pif_split_supported(self.handle))
+
+    def gather_split(self, id0: int = 0):
+        """Gather half of a split step: E at every particle (positions only;
+        the velocities may still be in flight) into a plan-owned (M,3) array,
+        row id - id0."""
+        cur = self._soa("cur")
+        _native.call("pif_interp_split", self.handle, ctypes.byref(cur),
+                     self.parts.perm.data_ptr(), int(id0), self._stream())
+        self.launches += 1
+
+    def push_rows(self, x, v, r0: int, r1: int):
+        """Push half: Boris push of rows [r0, r1) of id-ordered device (M,3)
+        x, v in place with the E rows of gather_split; the call reaching row M
+        writes the diagnostic sums."""
+        _native.call("pif_push_ids", self.handle, x.data_ptr(), v.data_ptr(), self.count,
+                     int(r0), int(r1 - r0), self.half, self.dt, self._tq, self._sq, self.has_b,
+                     self.e_kind, self.diag.data_ptr(), self._stream())
+        self.launches += 1 + (r1 == self.count)
+
     def rebin(self):
         """Scan the cell counts emitted by interp_push and rebuild perm."""
         if self.count:
@@ -436,12 +458,14 @@ class PifEngine:
         self.solve_fields()
 
     def run_host(self, xh, vh, id0: int, steps: int, energy_out=None, n_chunks: int = 16,
-                 trace=None):
+                 trace=None, split=None):
         """pif_step-style stepping of a host-resident ensemble (the reference's
         ParticleEnsemble use, pif.py:178-190): every step uploads x, v ((M,3),
         id order, ids id0 .. id0+M-1) from host memory, bins, deposits, reduces,
         solves, gathers + pushes, scatters back to id order and downloads x, v
         into the same host arrays (energy_out[s] <- the step's field energy).
+        split (default True for w <= 8): the gather runs before the velocities
+        arrive and only the streaming push waits for them.
 
         Positions travel first: binning, the deposit, the allreduce and the
         field solve of a step only need x, so they run while v is still being
@@ -455,6 +479,11 @@ class PifEngine:
         torch = require_cuda()
         M, dev = self.count, self.device
         scatter_after = os.environ.get("PIF_E2E_SCATTER", "0") == "1"
+        # split (default where the DMMA kernels run): gather E before the
+        # velocities arrive, push after; PIF_E2E_SPLIT=0 keeps the fused kernel
+        split = (split if split is not None else
+                 os.environ.get("PIF_E2E_SPLIT", "1") == "1") and not scatter_after \
+            and self.count > 0 and self.split_supported()
         if tuple(xh.shape) != (M, 3) or tuple(vh.shape) != (M, 3):
             raise ValueError(f"host arrays must be ({M}, 3)")
         main = torch.cuda.current_stream(dev)
@@ -474,6 +503,8 @@ class PifEngine:
             vd.copy_(vh, non_blocking=True)
             v_in = ev()
             v_in.record(up)
+        v_evs = [v_in] * len(bounds)   # split: per-chunk velocity arrivals
+
         def mark(stream):
             if trace is None:
                 return None
@@ -493,6 +524,47 @@ class PifEngine:
             t_dep = mark(main)
             self.allreduce()
             self.solve_fields()
+            if split:
+                # the gather needs positions only: it runs while v is in flight;
+                # then each row chunk is pushed as its velocities land and is
+                # downloaded as soon as its push ends
+                self.gather_split(id0)
+                t_fields = mark(main)
+                push_ev = []
+                for c, (i0, i1) in enumerate(bounds):
+                    main.wait_event(v_evs[c])
+                    if c == 0:
+                        t_v = mark(main)
+                    self.push_rows(xd, vd, i0, i1)
+                    e = ev()
+                    e.record(main)
+                    push_ev.append(e)
+                if energy_out is not None:
+                    energy_out[s:s + 1].copy_(self.scalars[0:1], non_blocking=True)
+                t_push = mark(main)
+                last = s == steps - 1
+                new_v = []
+                for src, dst_h, which in ((xd, xh, "x"), (vd, vh, "v")):
+                    for c, (i0, i1) in enumerate(bounds):
+                        down.wait_event(push_ev[c])
+                        with torch.cuda.stream(down):
+                            dst_h[i0:i1].copy_(src[i0:i1], non_blocking=True)
+                        if not last:
+                            up.wait_stream(down)
+                            with torch.cuda.stream(up):
+                                src[i0:i1].copy_(dst_h[i0:i1], non_blocking=True)
+                            if which == "v":
+                                e = ev()
+                                e.record(up)
+                                new_v.append(e)
+                    if not last and which == "x":
+                        x_in = ev()
+                        x_in.record(up)
+                v_evs = new_v
+                if trace is not None:
+                    trace.append((t_start, t_x, t_fields, t_v, t_push, mark(down), mark(up),
+                                  t_bin, t_perm, t_dep))
+                continue
             t_fields = mark(main)
             main.wait_event(v_in)
             t_v = mark(main)

@@ -599,6 +599,70 @@ def test_run_host_streaming_matches_pif_step(cuda):
     assert np.all(np.isfinite(wh.numpy())) and np.all(wh.numpy() > 0)
 
 
+@pytest.mark.parametrize("kind,ppm,det", [("landau", 64, True), ("penning", 16, True),
+                                          ("landau", 64, False)])
+def test_run_host_split_matches_fused(cuda, kind, ppm, det):
+    """run_host's split step (pif_interp_split before the velocities arrive,
+    then pif_push_ids row chunk by row chunk) against the fused gather+push
+    kernel: the same gather arithmetic and the same boris_one, so in the
+    deterministic mode the states are the same bits; by default the deposit's
+    atomics order differs between runs (rounding only)."""
+    import torch
+
+    from paper_2605_10729_b200.engine import PifEngine
+    spec = (pb.landau_spec if kind == "landau" else pb.penning_spec)(N=16, ppm=ppm, dt=0.05)
+    M = spec.num_particles
+    plan = pb.make_plan(spec.N, spec.L, 1e-7)
+    outs = []
+    for split in (False, True):
+        eng = PifEngine(plan, M, "cuda", q=spec.Q_e / M, m=-spec.Q_e / M,
+                        externals=spec.externals(), dt=spec.dt, deterministic=det)
+        assert eng.split_supported()
+        eng.load_sampled(spec, (0, M))
+        xd, vd = eng.to_id_order()
+        xh, vh = xd.cpu().pin_memory(), vd.cpu().pin_memory()
+        wh = torch.zeros(3, dtype=torch.float64).pin_memory()
+        eng.run_host(xh, vh, 0, 3, energy_out=wh, n_chunks=5, split=split)
+        torch.cuda.synchronize()
+        outs.append((xh.clone(), vh.clone(), wh.clone(), eng.diag[0:5].cpu().clone()))
+    (x0, v0, w0, d0), (x1, v1, w1, d1) = outs
+    if det:
+        assert torch.equal(x0, x1) and torch.equal(v0, v1) and torch.equal(w0, w1)
+    else:
+        assert rel_max(x1.numpy(), x0.numpy()) <= 1e-12
+        assert rel_max(v1.numpy(), v0.numpy()) <= 1e-12
+        assert rel_max(w1.numpy(), w0.numpy()) <= 1e-12
+    assert rel_max(d1.numpy(), d0.numpy()) <= 1e-12
+
+
+def test_push_ids_needs_its_gather(cuda):
+    """pif_push_ids refuses rows without the split gather of the same set, and
+    the gather is consumed once every row is pushed."""
+    import torch
+
+    from paper_2605_10729_b200 import _native
+    from paper_2605_10729_b200.engine import PifEngine
+    spec = pb.landau_spec(N=8, ppm=8, dt=0.05)
+    M = spec.num_particles
+    eng = PifEngine(pb.make_plan(spec.N, spec.L, 1e-7), M, "cuda", q=spec.Q_e / M,
+                    m=-spec.Q_e / M, externals=spec.externals(), dt=spec.dt)
+    eng.load_sampled(spec, (0, M))
+    x, v = eng.to_id_order()
+    eng.deposit()
+    eng.solve_fields()
+    with pytest.raises(_native.NativeError, match="split gather"):
+        eng.push_rows(x, v, 0, M)
+    eng.gather_split(0)
+    eng.push_rows(x, v, 0, M // 3)
+    eng.push_rows(x, v, M // 3, M)      # reaches row M: diag written, gather consumed
+    with pytest.raises(_native.NativeError, match="split gather"):
+        eng.push_rows(x, v, 0, M)
+    with pytest.raises(ValueError):
+        _native.call("pif_push_ids", eng.handle, x.data_ptr(), v.data_ptr(), M, 5, M, 0.1, 0.1,
+                     eng._tq, eng._sq, 0, 0, eng.diag.data_ptr(), eng._stream())
+    torch.cuda.synchronize()
+
+
 @pytest.mark.parametrize("eps,N,M", [(1e-9, 8, 20000), (1e-12, 8, 20000), (1e-13, 12, 70000),
                                      (1e-14, 12, 70000), (1e-15, 12, 70000),
                                      (1e-16, 12, 70000)])
