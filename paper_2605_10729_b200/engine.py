@@ -504,6 +504,23 @@ class PifEngine:
             v_in = ev()
             v_in.record(up)
         v_evs = [v_in] * len(bounds)   # split: per-chunk velocity arrivals
+        # The step's energy leaves by the download stream after that step's
+        # x, v chunks: a small D2H on the compute stream would queue on the
+        # copy engine behind gigabytes of downloads and stall the next step.
+        # It is first copied on the compute stream (an elementwise kernel, not
+        # the copy engine) into a per-step device slot.
+        ehist = (torch.empty(steps, dtype=torch.float64, device=dev)
+                 if energy_out is not None else None)
+
+        def keep_energy(s):
+            if ehist is not None:
+                torch.mul(self.scalars[0:1], 1.0, out=ehist[s:s + 1])
+
+        def send_energy(s):
+            if ehist is not None:
+                down.wait_stream(main)
+                with torch.cuda.stream(down):
+                    energy_out[s:s + 1].copy_(ehist[s:s + 1], non_blocking=True)
 
         def mark(stream):
             if trace is None:
@@ -539,8 +556,7 @@ class PifEngine:
                     e = ev()
                     e.record(main)
                     push_ev.append(e)
-                if energy_out is not None:
-                    energy_out[s:s + 1].copy_(self.scalars[0:1], non_blocking=True)
+                keep_energy(s)
                 t_push = mark(main)
                 last = s == steps - 1
                 new_v = []
@@ -560,6 +576,7 @@ class PifEngine:
                     if not last and which == "x":
                         x_in = ev()
                         x_in.record(up)
+                send_energy(s)
                 v_evs = new_v
                 if trace is not None:
                     trace.append((t_start, t_x, t_fields, t_v, t_push, mark(down), mark(up),
@@ -582,8 +599,7 @@ class PifEngine:
                     self.gather_push()
                 finally:
                     _native.call("pif_set_id_order_output", self.handle, None, None, 0)
-            if energy_out is not None:
-                energy_out[s:s + 1].copy_(self.scalars[0:1], non_blocking=True)
+            keep_energy(s)
             t_push = mark(main)
             down.wait_stream(main)
             last = s == steps - 1
@@ -602,6 +618,7 @@ class PifEngine:
                         x_in = e
                     else:
                         v_in = e
+            send_energy(s)
             if trace is not None:
                 trace.append((t_start, t_x, t_fields, t_v, t_push, mark(down), mark(up), t_bin,
                               t_perm, t_dep))

@@ -27,12 +27,13 @@ vh = torch.empty((M, 3), dtype=torch.float64, pin_memory=True)
 xh.copy_(xd0)
 vh.copy_(vd0)
 del xd0, vd0
-eng.run_host(xh, vh, 0, 1, n_chunks=chunks)
+wh = torch.empty(4, dtype=torch.float64, pin_memory=True)   # as bench.py: W per step
+eng.run_host(xh, vh, 0, 1, energy_out=wh, n_chunks=chunks)
 torch.cuda.synchronize()
 tr = []
 t0 = torch.cuda.Event(enable_timing=True)
 t0.record()
-eng.run_host(xh, vh, 0, 4, n_chunks=chunks, trace=tr)
+eng.run_host(xh, vh, 0, 4, energy_out=wh, n_chunks=chunks, trace=tr)
 torch.cuda.synchronize()
 print(f"M = 2^{lm}, {chunks} chunks; ms from the first step's start")
 names = ("start", "x in", "fields", "v in", "push", "D2H end", "H2D end")
