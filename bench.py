@@ -29,9 +29,6 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-# before CUDA initialises: separate hardware queues for the e2e copy streams
-# (paper_2605_10729_b200/__init__.py)
-os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 METRIC = "particle-steps/sec (Landau 3D-3V, 64^3 modes) at 1/2/4/8 B200; % roofline"
 UNIT = "particle-steps/s"
