@@ -211,7 +211,7 @@ def run_reference(a):
                          "extrapolated_full_size": r["extrapolated"]},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ---------------------------------------------------------------------------
@@ -410,7 +410,7 @@ def run_b200(a):
             "config": cfg, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -474,7 +474,22 @@ def run_e2e(a, eng, torch, dist, world, per_gpu, glob, dev):
                    "step s+1's H2D chunk-pipelined"}
 
 
+_JSON_OUT = None
+
+
+def emit(line: dict) -> None:
+    """The one JSON line, on the original stdout."""
+    out = _JSON_OUT or sys.stdout
+    print(json.dumps(line), file=out, flush=True)
+
+
 def main():
+    # stdout carries exactly the JSON line: anything else written to fd 1
+    # (NCCL's version banner under torchrun, library chatter) goes to stderr
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     a = parse()
     if a.impl == "reference":
         run_reference(a)

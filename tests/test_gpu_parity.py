@@ -611,18 +611,20 @@ def test_run_host_split_matches_fused(cuda, kind, ppm, det):
 
     from paper_2605_10729_b200.engine import PifEngine
     spec = (pb.landau_spec if kind == "landau" else pb.penning_spec)(N=16, ppm=ppm, dt=0.05)
-    M = spec.num_particles
+    n = spec.num_particles
+    lo = 0 if kind == "landau" else 777     # a rank's id slice: rows are ids - lo
+    M = n - lo
     plan = pb.make_plan(spec.N, spec.L, 1e-7)
     outs = []
     for split in (False, True):
-        eng = PifEngine(plan, M, "cuda", q=spec.Q_e / M, m=-spec.Q_e / M,
+        eng = PifEngine(plan, M, "cuda", q=spec.Q_e / n, m=-spec.Q_e / n,
                         externals=spec.externals(), dt=spec.dt, deterministic=det)
         assert eng.split_supported()
-        eng.load_sampled(spec, (0, M))
-        xd, vd = eng.to_id_order()
+        eng.load_sampled(spec, (lo, n))
+        xd, vd = eng.to_id_order(id0=lo)
         xh, vh = xd.cpu().pin_memory(), vd.cpu().pin_memory()
         wh = torch.zeros(3, dtype=torch.float64).pin_memory()
-        eng.run_host(xh, vh, 0, 3, energy_out=wh, n_chunks=5, split=split)
+        eng.run_host(xh, vh, lo, 3, energy_out=wh, n_chunks=5, split=split)
         torch.cuda.synchronize()
         outs.append((xh.clone(), vh.clone(), wh.clone(), eng.diag[0:5].cpu().clone()))
     (x0, v0, w0, d0), (x1, v1, w1, d1) = outs
