@@ -185,6 +185,14 @@ int pif_push_ids(pif_plan_t plan, double *x, double *v, int64_t M, int64_t row0,
                  double half, double dt, const double tq[3], const double sq[3], int has_b,
                  int e_kind, double *diag, void *stream);
 int pif_split_supported(pif_plan_t plan);
+/* Sparse sets (a few particles per stencil cell): the DMMA spread can walk C
+ * x-adjacent columns as one super-column (fewer plane flushes and REDs, fuller
+ * k-steps, (C+7)/8 of the DMMAs per k-step; spread_r, _kernels.py:57-96, same
+ * sums).  c = -1: by density (default; env PIF_SPREAD_MERGE overrides at plan
+ * creation), 0 or 1: never, 2 or 4: always (w = 6..8, n >= 32, not in the
+ * deterministic mode).  pif_spread_merge_used: the C of the last spread. */
+int pif_set_spread_merge(pif_plan_t plan, int c);
+int pif_spread_merge_used(pif_plan_t plan);
 /* Gather only (gather_efield): E at the sorted particles written to
  * E_out[3*id + d] (AoS, particle id order). */
 int pif_interp_sorted(pif_plan_t plan, const pif_soa_t *sorted, double *E_out, void *stream);

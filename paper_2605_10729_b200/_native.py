@@ -65,6 +65,8 @@ SIGNATURES = {
     "pif_interp_split": ([_P, _SOA, _P, _I64, _P], _I),
     "pif_push_ids": ([_P, _P, _P, _I64, _I64, _I64, _D, _D, _D3, _D3, _I, _I, _P, _P], _I),
     "pif_split_supported": ([_P], _I),
+    "pif_set_spread_merge": ([_P, _I], _I),
+    "pif_spread_merge_used": ([_P], _I),
     "pif_grid_to_modes": ([_P, _P, _P], _I),
     "pif_solve_fields": ([_P, _P, _I, _P, _P, _P], _I),
     "pif_fields_from_modes": ([_P, _P, _P, _P, _I, _P, _P], _I),

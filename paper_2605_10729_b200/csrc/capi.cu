@@ -55,7 +55,8 @@ void release(Plan &p) {
     void *ptrs[] = {p.deconv, p.kvec, p.grid, p.spec, p.field, p.field3, p.emodes, p.cgrid,
                     p.cell_count, p.cell_start, p.scan_tmp, p.work, p.partials, p.maxbits,
                     p.shape_tab, p.items, p.seg_parts, p.seg_off, p.max_parts, p.ring_scratch, p.wcache,
-                    p.dbuf, p.det_keys, p.det_iota, p.det_tmp};
+                    p.dbuf, p.det_keys, p.det_iota, p.det_tmp, p.cell_start2, p.perm2,
+                    p.items2, p.seg_parts2, p.seg_off2};
     for (void *q : ptrs)
         if (q) cudaFree(q);
     if (p.max_parts_host) cudaFreeHost(p.max_parts_host);
@@ -214,6 +215,7 @@ int pif_plan_create(const pif_plan_desc_t *d, int device, pif_plan_t *out) {
     if (const char *pa = std::getenv("PIF_PUSH_AGG")) p.push_agg_force = std::atoi(pa) != 0;
     if (const char *rs = std::getenv("PIF_RING_SPREAD_MIN")) p.ring_spread_min = std::atof(rs);
     if (const char *rg = std::getenv("PIF_RING_GATHER_MIN")) p.ring_gather_min = std::atof(rg);
+    if (const char *sm = std::getenv("PIF_SPREAD_MERGE")) p.merge_force = std::atoi(sm);
     int rc = PIF_OK;
 #define TRY(x)                    \
     do {                          \
@@ -420,6 +422,19 @@ int pif_push_ids(pif_plan_t plan, double *x, double *v, int64_t M, int64_t row0,
     if (!(dt > 0)) return pif::bad("dt must be positive");
     return pif::launch_push_ids(p, x, v, M, row0, row0 + rows, half, dt, tq, sq, has_b, e_kind,
                                 diag, s);
+}
+
+int pif_set_spread_merge(pif_plan_t plan, int c) {
+    if (!plan) return pif::bad("null plan");
+    if (c != -1 && c != 0 && c != 1 && c != 2 && c != 4)
+        return pif::bad("spread merge factor must be -1 (auto), 0/1 (off), 2 or 4");
+    plan->p.merge_force = c;
+    return PIF_OK;
+}
+
+int pif_spread_merge_used(pif_plan_t plan) {
+    if (!plan) return pif::bad("null plan");
+    return plan->p.merge_used;
 }
 
 int pif_split_supported(pif_plan_t plan) {

@@ -552,6 +552,267 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
     }
 }
 
+// ----------------------------------------------------------------------------
+// merged-column spreading for sparse sets
+//
+// At a few particles per stencil cell the column kernel above pays per cell
+// step, not per particle: every cell step flushes a full 8 x 8 plane (so the
+// grid receives 64 REDs per point and step whatever the density) and most
+// k-steps of 4 particles are ragged.  Walking C x-adjacent columns as one
+// super-column divides the cell steps and plane flushes by C, the REDs per
+// grid point by 64 C / (8 (C + 7)) and the ragged steps by about C, for
+// (C + 7) / 8 times the DMMAs per k-step: a particle of sub-column
+// q = i0x - ix0 occupies union rows a' = q .. q + 7, i.e. its (strength-scaled)
+// wx row is shifted by q and zero elsewhere, so one k-step mixes sub-columns.
+// The super-columns have their own cell order,
+//   mk = (((kx / C) n + ky) n + kz) C + kx mod C,
+// in which a super-column's C cells of level kz are consecutive; cell_start2,
+// perm2 and the work items are derived from the standard binning before each
+// merged spread (merged_counts / scan / merged_perm / merged_seg_parts).
+// ----------------------------------------------------------------------------
+
+__device__ __forceinline__ int64_t merged_cell(int k, int n, int C) {
+    const int kz = k % n, t = k / n, ky = t % n, kx = t / n;
+    return ((((int64_t)(kx / C) * n + ky) * n + kz) * C) + kx % C;
+}
+
+// count2[mk] = size of the standard cell behind merged cell mk; count2[n^3] = 0
+__global__ void merged_counts_kernel(const int32_t *__restrict__ cell_start, int n, int C,
+                                     int32_t *__restrict__ count2) {
+    const int64_t n3 = (int64_t)n * n * n;
+    for (int64_t mk = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; mk <= n3;
+         mk += (int64_t)gridDim.x * blockDim.x) {
+        if (mk == n3) {
+            count2[mk] = 0;
+            continue;
+        }
+        const int q = (int)(mk % C);
+        int64_t t = mk / C;
+        const int kz = (int)(t % n);
+        t /= n;
+        const int ky = (int)(t % n);
+        const int mx = (int)(t / n);
+        const int64_t k = ((int64_t)(mx * C + q) * n + ky) * n + kz;
+        count2[mk] = cell_start[k + 1] - cell_start[k];
+    }
+}
+
+// perm2: a standard cell's particles keep their slot order inside their merged
+// cell; the cell comes from the particle's position (the binning's own key)
+__global__ void merged_perm_kernel(const double *__restrict__ px, const double *__restrict__ py,
+                                   const double *__restrict__ pz,
+                                   const int32_t *__restrict__ perm,
+                                   const int32_t *__restrict__ cell_start,
+                                   const int32_t *__restrict__ cell_start2, int64_t M, double h,
+                                   int w, int n, int C, int32_t *__restrict__ perm2) {
+    const double rh = __drcp_rn(h);
+    for (int64_t slot = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; slot < M;
+         slot += (int64_t)gridDim.x * blockDim.x) {
+        const int j = perm ? perm[slot] : (int)slot;
+        const int k = cell_key(px[j], py[j], pz[j], h, rh, w, n);
+        PIF_CHECK(slot >= cell_start[k] && slot < cell_start[k + 1]);
+        perm2[cell_start2[merged_cell(k, n, C)] + (slot - cell_start[k])] = j;
+    }
+}
+
+// parts of <= kItemParticles particles of each non-empty segment of seg levels
+// of a super-column (C n consecutive merged cells)
+__global__ void merged_seg_parts_kernel(const int32_t *__restrict__ cell_start2, int n, int C,
+                                        int seg, int nseg, int nsegs, int *__restrict__ parts) {
+    for (int sidx = blockIdx.x * blockDim.x + threadIdx.x; sidx <= nsegs;
+         sidx += gridDim.x * blockDim.x) {
+        if (sidx == nsegs) {
+            parts[sidx] = 0;
+            continue;
+        }
+        const int col = sidx / nseg, sg = sidx - col * nseg;
+        const int64_t base = (int64_t)col * C * n;
+        const int k0 = sg * seg, k1 = min(k0 + seg, n);
+        const int c = cell_start2[base + (int64_t)k1 * C] - cell_start2[base + (int64_t)k0 * C];
+        parts[sidx] = (c + kItemParticles - 1) / kItemParticles;
+    }
+}
+
+template <int NA>
+struct MergedChunk {
+    double wx[NA][kChunk + 1];   // union x rows a' (times the strength)
+    double wy[kChunk][9];        // [p][b]
+    double wz[8][kWzStride];     // [c][p]
+};
+
+// this lane's particle: per-axis weights (es_fast.cuh), the x row shifted to
+// the particle's sub-column q = i0x - ix0
+template <int W, int NA>
+__device__ __forceinline__ void merged_weights(MergedChunk<NA> &st, const double *tab,
+                                               const EsPoly &P, int lane, int cnt, double x,
+                                               double y, double z, double s, double h, double rh,
+                                               double beta, int ix0, int n) {
+    if (lane < cnt) {
+        const double cx = axis_coord(x, h, rh);
+        const int q = cell_index_of(cx, W, n) - ix0;
+        PIF_CHECK(q >= 0 && q + 8 <= NA);
+        double wt[W];
+        es_axis_weights<W>(cx, beta, P, tab, wt);
+#pragma unroll
+        for (int a = 0; a < NA; ++a) st.wx[a][lane] = 0.0;
+#pragma unroll
+        for (int a = 0; a < W; ++a) st.wx[a + q][lane] = __dmul_rn(s, wt[a]);
+        es_axis_weights<W>(axis_coord(y, h, rh), beta, P, tab, wt);
+#pragma unroll
+        for (int a = 0; a < W; ++a) st.wy[lane][a] = wt[a];
+        es_axis_weights<W>(axis_coord(z, h, rh), beta, P, tab, wt);
+#pragma unroll
+        for (int a = 0; a < W; ++a) st.wz[a][lane] = wt[a];
+    }
+    __syncwarp();
+}
+
+template <int NA>
+__device__ __forceinline__ void merged_flush_plane(double (&acc)[NA][2], int k, int c4, int ix0,
+                                                   int64_t yrow, int n, double *grid) {
+    const int s = k & 7;
+    if (c4 == (s >> 1)) {
+        const int j = s & 1;
+#pragma unroll
+        for (int a = 0; a < NA; ++a) {
+            const double v = j ? acc[a][1] : acc[a][0];
+            int xa = ix0 + a;
+            xa = xa >= n ? xa - n : xa;   // n >= 32 > NA (merged_factor)
+            if (v != 0.0) atomicAdd(grid + ((int64_t)xa * n + yrow) * n + k, v);
+            if (j) acc[a][1] = 0.0;
+            else acc[a][0] = 0.0;
+        }
+    }
+}
+
+// spread_mma_kernel over super-columns (same chunks, k-steps, z-slot planes
+// and flush order per plane), NA = C + 7 union x rows per k-step
+template <int W, int C>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, PIF_SPREAD_MINB)
+spread_merged_kernel(const double *__restrict__ px, const double *__restrict__ py,
+                     const double *__restrict__ pz, const int64_t *__restrict__ pid,
+                     const int32_t *__restrict__ perm2, const double *__restrict__ strengths,
+                     double q, const int32_t *__restrict__ cell_start2, double *__restrict__ grid,
+                     int n, int seg, int nseg, double h, double beta, const EsPoly poly,
+                     unsigned int *work, const int2 *__restrict__ items,
+                     const int *__restrict__ n_items) {
+    constexpr int NA = C + 7;
+    const int nitems = *n_items;
+    const double rh = __drcp_rn(h);
+    __shared__ MergedChunk<NA> stage[kWarpsPerBlock];
+    __shared__ double tab[32];
+    __shared__ int seg_cells[kWarpsPerBlock][kMaxSeg + 1];
+    if (threadIdx.x < 32) tab[threadIdx.x] = kExp2Table[threadIdx.x];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    MergedChunk<NA> &st = stage[threadIdx.x >> 5];
+    int *cbt = seg_cells[threadIdx.x >> 5];
+    {
+        double *wp = &st.wx[0][0];
+        const int nw = (int)(sizeof(MergedChunk<NA>) / sizeof(double));
+        for (int i = lane; i < nw; i += 32) wp[i] = 0.0;
+        __syncwarp();
+    }
+    const int r = lane >> 2, c4 = lane & 3;
+
+    for (;;) {
+        int item = 0;
+        if (lane == 0) item = (int)atomicAdd(work, 1u);
+        item = __shfl_sync(kFull, item, 0);
+        if (item >= nitems) break;
+        const int2 it = items[item];
+        const int col = it.x / nseg, sg = it.x - col * nseg;
+        const int mx = col / n, iy = col - mx * n;
+        const int ix0 = mx * C;
+        const int k0 = sg * seg, k1 = min(k0 + seg, n);
+        const int64_t base = (int64_t)col * C * n;
+        __syncwarp();   // the previous item is done with the level table
+        for (int c = lane; c <= k1 - k0; c += 32) cbt[c] = cell_start2[base + (int64_t)(k0 + c) * C];
+        __syncwarp();
+        const int pbeg = cbt[0] + it.y * kItemParticles;
+        const int pend = min(pbeg + kItemParticles, cbt[k1 - k0]);
+        const int64_t yrow = (iy + r) % n;
+
+        double acc[NA][2];
+#pragma unroll
+        for (int a = 0; a < NA; ++a) acc[a][0] = acc[a][1] = 0.0;
+        int k = k0;
+        int cell_end = cbt[1];
+        while (cell_end <= pbeg) cell_end = cbt[(++k) - k0 + 1];
+
+        double nx = 0.0, ny = 0.0, nz = 0.0, ns = q;
+        if (pbeg + lane < pend) {
+            const int i = perm2[pbeg + lane];
+            nx = px[i];
+            ny = py[i];
+            nz = pz[i];
+            if (strengths) ns = strengths[pid[i]];
+        }
+        int npi = -1;
+        if (pbeg + kChunk + lane < pend) npi = perm2[pbeg + kChunk + lane];
+        for (int pos = pbeg; pos < pend; pos += kChunk) {
+            const int cnt = min(kChunk, pend - pos);
+            const double cx = nx, cy = ny, cz = nz, cs = ns;
+            if (npi >= 0) {
+                nx = px[npi];
+                ny = py[npi];
+                nz = pz[npi];
+                if (strengths) ns = strengths[pid[npi]];
+            }
+            npi = -1;
+            if (pos + 2 * kChunk + lane < pend) npi = perm2[pos + 2 * kChunk + lane];
+            merged_weights<W, NA>(st, tab, poly, lane, cnt, cx, cy, cz, cs, h, rh, beta, ix0, n);
+            int j = 0;
+            while (j < cnt) {
+                if (pos + j >= cell_end) {
+                    merged_flush_plane<NA>(acc, k, c4, ix0, yrow, n, grid);
+                    ++k;
+                    cell_end = cbt[k - k0 + 1];
+                    continue;
+                }
+                const int jend = min(cnt, cell_end - pos);
+                const int zs = (r - k) & 7;
+                PIF_CHECK(jend <= kChunk && k >= k0 && k < k1);
+#pragma unroll kSpreadUnroll
+                for (; j + 4 <= jend; j += 4) {
+                    const int pj = j + c4;
+                    const double wyb = st.wy[pj][r];
+                    const double bz = st.wz[zs][pj];
+#pragma unroll
+                    for (int a = 0; a < NA; ++a)
+                        dmma884(acc[a][0], acc[a][1], st.wx[a][pj] * wyb, bz);
+                }
+                if (j < jend) {
+                    const bool ok = c4 < jend - j;
+                    const int pj = ok ? j + c4 : j;
+                    const double wyb = ok ? st.wy[pj][r] : 0.0;
+                    const double bz = st.wz[zs][pj];
+#pragma unroll
+                    for (int a = 0; a < NA; ++a)
+                        dmma884(acc[a][0], acc[a][1], st.wx[a][pj] * wyb, bz);
+                    j = jend;
+                }
+            }
+            __syncwarp();
+        }
+        for (; k < k1; ++k) merged_flush_plane<NA>(acc, k, c4, ix0, yrow, n, grid);
+        // pending planes k1 .. k1+6
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+            const int sl = 2 * c4 + jj;
+            const int dz = (sl - k1) & 7;   // dz == 7: plane k1 + 7, flushed with cell k1 - 1
+            const int z = (k1 + dz) % n;
+#pragma unroll
+            for (int a = 0; a < NA; ++a) {
+                const double v = acc[a][jj];
+                int xa = ix0 + a;
+                xa = xa >= n ? xa - n : xa;
+                if (v != 0.0) atomicAdd(grid + ((int64_t)xa * n + yrow) * n + z, v);
+            }
+        }
+    }
+}
+
 // Deterministic plane reduction: grid point (X, Y, Z) = sum over the footprint
 // rows (a, b) of column (X - a, Y - b), over the z-segments of that column
 // whose footprint [k0, k1 + 7) covers Z (cyclically), over each segment's
@@ -2088,6 +2349,121 @@ int launch_bin_perm(Plan &p, const int32_t *key, const int32_t *rank, int64_t M,
                      "reset cell counts");
 }
 
+// Merged-column spread (spread_merged_kernel) below these densities
+// (particles per stencil cell) when the weight cache is off: C = 4, then
+// C = 2; above, the column kernel (256^3 / 1.25 per cell: spread 59.4 ms ->
+// 43.1 (C = 2) -> 33.6 (C = 4); profiles/round2/spread_merge_ab.txt).
+#ifndef PIF_MERGE4_BELOW
+#define PIF_MERGE4_BELOW 3.0
+#endif
+#ifndef PIF_MERGE2_BELOW
+#define PIF_MERGE2_BELOW 12.0
+#endif
+
+int merged_factor(const Plan &p) {
+    if (p.det || p.n < 32 || p.w < 6 || !fast_path_ok(p)) return 1;
+    if (p.merge_force >= 0) return p.merge_force >= 2 ? p.merge_force : 1;
+    // the merged order cannot feed the gather's weight cache (its slots are in
+    // the column order), and from 4 per cell the cache is worth more (128^3 /
+    // 8 per cell: spread -1.0 ms merged, gather +1.9 ms without the cache)
+    if (p.wcache_on) return 1;
+    if (p.density < PIF_MERGE4_BELOW) return 4;
+    if (p.density < PIF_MERGE2_BELOW) return 2;
+    return 1;
+}
+
+template <typename T>
+int grow(T **ptr, int64_t &cap, int64_t need, const char *what) {
+    if (need <= cap) return PIF_OK;
+    if (*ptr) cudaFree(*ptr);
+    *ptr = nullptr;
+    cap = 0;
+    const cudaError_t e = cudaMalloc(reinterpret_cast<void **>(ptr), sizeof(T) * need);
+    if (e != cudaSuccess) return fail_cuda(e, what);
+    cap = need;
+    return PIF_OK;
+}
+
+// super-column cell order, perm and work items from the standard binning
+// (p.cell_start of perm); returns the merged segment length / count
+int build_merged(Plan &p, const pif_soa_t &P, const int32_t *perm, int C, int &seg, int &nseg,
+                 int &nsegs, cudaStream_t s) {
+    const int64_t n3 = p.n3, M = P.count;
+    if (!p.cell_start2) {
+        const cudaError_t e =
+            cudaMalloc(reinterpret_cast<void **>(&p.cell_start2), sizeof(int32_t) * 2 * (n3 + 1));
+        if (e != cudaSuccess) return fail_cuda(e, "merged cell table");
+    }
+    int32_t *count2 = p.cell_start2, *cs2 = p.cell_start2 + (n3 + 1);
+    if (grow(&p.perm2, p.perm2_cap, M, "merged perm") != PIF_OK) return PIF_ERR_CUDA;
+    merged_counts_kernel<<<grid_for(n3 + 1, 256, p.sm_count), 256, 0, s>>>(p.cell_start, p.n, C,
+                                                                           count2);
+    size_t tmp = p.scan_tmp_bytes;
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(p.scan_tmp, tmp, count2, cs2, (int)(n3 + 1), s);
+    if (e != cudaSuccess) return fail_cuda(e, "merged cell scan");
+    merged_perm_kernel<<<grid_for(M, 256, p.sm_count), 256, 0, s>>>(
+        P.x, P.y, P.z, perm, p.cell_start, cs2, M, p.h, p.w, p.n, C, p.perm2);
+    // segments of seg levels holding ~seg_target particles, as segment_cells
+    const double per_level = p.density * C;
+    seg = (int)std::ceil((double)p.seg_target / (per_level > 1.0 ? per_level : 1.0));
+    seg = seg < 8 ? 8 : (seg > kMaxSeg ? kMaxSeg : seg);
+    nseg = (p.n + seg - 1) / seg;
+    nsegs = (p.n / C) * p.n * nseg;
+    if (p.segs2_cap < (int64_t)nsegs + 1) {
+        if (p.seg_parts2) cudaFree(p.seg_parts2);
+        if (p.seg_off2) cudaFree(p.seg_off2);
+        p.seg_parts2 = p.seg_off2 = nullptr;
+        p.segs2_cap = 0;
+        e = cudaMalloc(reinterpret_cast<void **>(&p.seg_parts2), sizeof(int) * (nsegs + 1));
+        if (e == cudaSuccess)
+            e = cudaMalloc(reinterpret_cast<void **>(&p.seg_off2), sizeof(int) * (nsegs + 1));
+        if (e != cudaSuccess) return fail_cuda(e, "merged segment tables");
+        p.segs2_cap = nsegs + 1;
+    }
+    if (grow(&p.items2, p.items2_cap, (int64_t)nsegs + M / kItemParticles + 1,
+             "merged work items") != PIF_OK)
+        return PIF_ERR_CUDA;
+    merged_seg_parts_kernel<<<grid_for(nsegs + 1, 256, p.sm_count), 256, 0, s>>>(
+        cs2, p.n, C, seg, nseg, nsegs, p.seg_parts2);
+    tmp = p.scan_tmp_bytes;
+    e = cub::DeviceScan::ExclusiveSum(p.scan_tmp, tmp, p.seg_parts2, p.seg_off2, nsegs + 1, s);
+    if (e != cudaSuccess) return fail_cuda(e, "merged segment scan");
+    seg_items_kernel<<<grid_for(nsegs, 256, p.sm_count), 256, 0, s>>>(p.seg_parts2, p.seg_off2,
+                                                                      nsegs, p.items2);
+    return fail_cuda(cudaGetLastError(), "merged binning kernels");
+}
+
+int launch_spread_merged(Plan &p, const pif_soa_t &P, const int32_t *perm,
+                         const double *strengths, double q, int C, cudaStream_t s) {
+    int seg = 0, nseg = 0, nsegs = 0;
+    int rc = build_merged(p, P, perm, C, seg, nseg, nsegs, s);
+    if (rc != PIF_OK) return rc;
+    cudaError_t e = cudaMemsetAsync(p.work, 0, sizeof(unsigned int), s);
+    if (e != cudaSuccess) return fail_cuda(e, "zero work counter");
+    const EsPoly poly = device_poly(p);
+    const int threads = kWarpsPerBlock * 32;
+    const int32_t *cs2 = p.cell_start2 + (p.n3 + 1);
+    const int *nitems = p.seg_off2 + nsegs;
+#define PIF_MERGED_CASE(W, CC)                                                                 \
+    if (p.w == W && C == CC) {                                                                 \
+        auto k = spread_merged_kernel<W, CC>;                                                  \
+        const int blocks = persistent_blocks(k, threads, 0, p.sm_count);                      \
+        k<<<blocks, threads, 0, s>>>(P.x, P.y, P.z, P.id, p.perm2, strengths, q, cs2, p.grid,  \
+                                     p.n, seg, nseg, p.h, p.beta, poly, p.work, p.items2,     \
+                                     nitems);                                                  \
+        return fail_cuda(cudaGetLastError(), "spread_merged_kernel");                          \
+    }
+    PIF_MERGED_CASE(8, 2)
+    PIF_MERGED_CASE(8, 4)
+    PIF_MERGED_CASE(7, 2)
+    PIF_MERGED_CASE(7, 4)
+    PIF_MERGED_CASE(6, 2)
+    PIF_MERGED_CASE(6, 4)
+#undef PIF_MERGED_CASE
+    set_error("merged spread: w = 6..8 and C = 2 or 4 only");
+    return PIF_ERR_STATE;
+}
+
 int launch_spread(Plan &p, const pif_soa_t &P, const int32_t *perm, const double *strengths,
                   double q, cudaStream_t s) {
     const EsPoly poly = device_poly(p);
@@ -2095,7 +2471,13 @@ int launch_spread(Plan &p, const pif_soa_t &P, const int32_t *perm, const double
     if (e != cudaSuccess) return fail_cuda(e, "zero grid");
     if (P.count == 0) return PIF_OK;
     p.wcache_valid = false;
+    p.merge_used = 1;
     if (fast_path_ok(p)) {
+        const int C = merged_factor(p);
+        if (C > 1) {
+            p.merge_used = C;
+            return launch_spread_merged(p, P, perm, strengths, q, C, s);
+        }
         const int nseg = (p.n + p.seg - 1) / p.seg;
         const int *nitems = p.seg_off + p.n_segs;
         e = cudaMemsetAsync(p.work, 0, sizeof(unsigned int), s);

@@ -318,6 +318,15 @@ class PifEngine:
         if self.deterministic:      # the fused sums depend on the work-item schedule
             self.particle_diag()
 
+    def set_spread_merge(self, c: int):
+        """Merged-column spread for sparse sets: -1 by density (default), 0 off,
+        2 or 4 columns per super-column (pif_set_spread_merge)."""
+        _native.call("pif_set_spread_merge", self.handle, int(c))
+
+    def spread_merge_used(self) -> int:
+        """Columns per super-column of the last spread (1: the column kernel)."""
+        return int(_native.load().pif_spread_merge_used(self.handle))
+
     def split_supported(self) -> bool:
         """pif_interp_split / pif_push_split cover the DMMA kernels (w <= 8)."""
         return bool(_native.load().pif_split_supported(self.handle))

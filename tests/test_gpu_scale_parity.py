@@ -178,3 +178,49 @@ def test_cic_deposit_and_gather_api_match_oracle(cuda):
     E = pb.gather_efield(*pb.poisson_efield(rho), ens, plan, "cic")
     E_o = o.gather_efield(o.poisson_efield(rho_o, spec.L), ens.x, op, "cic")
     assert rel_l2(E, E_o) <= TIGHT
+
+
+MERGE_CASES = [(eps, ppc) for eps in (1e-5, 1e-6, 1e-7) for ppc in (0.3, 1.25, 8.0)]
+
+
+@pytest.mark.parametrize("eps,ppc", MERGE_CASES, ids=[f"eps{e:g}-{p}percell" for e, p in
+                                                      MERGE_CASES])
+def test_merged_column_spread_matches_oracle(eps, ppc, cuda):
+    """The merged-column spread (C = 2 and 4 x-adjacent columns per
+    super-column, pif_set_spread_merge) gives the oracle's rho_hat at sparse
+    and moderate densities for w = 6, 7, 8, like the column kernel (C = 1), and
+    the density rule picks it where it should."""
+    torch = cuda
+    from paper_2605_10729_b200.engine import PifEngine
+    o = oracle()
+    N, L = 16, 4 * np.pi                     # fine grid n = 32
+    plan = pb.make_plan(N, L, eps)
+    op = o.make_plan(N, L, eps)
+    assert plan.window.w == {1e-5: 6, 1e-6: 7, 1e-7: 8}[eps]
+    M = int(ppc * 32 ** 3)
+    rng = np.random.default_rng(M)
+    x = rng.random((M, 3)) * L
+    x[:5] = [[0.0, 0.0, 0.0], [L - 1e-13, 1e-14, 0.5 * L], [plan.h, 2 * plan.h, L - plan.h],
+             [L * 0.999999, L * 0.999999, L * 0.999999], [0.5 * L, 0.5 * L, 0.5 * L]]
+    q = -1.0 / M
+    dev = torch.device("cuda", 0)
+    xt = torch.tensor(x, device=dev)
+    rho_o = _oracle_rho(o, op, x, q, "delta", _threads())
+    got = {}
+    for c in (0, 2, 4, -1):
+        eng = PifEngine(plan, M, dev, q=q, m=1.0 / M, dt=0.05,
+                        externals=pb.landau_spec(N=N, ppm=1).externals())
+        eng.load(xt, torch.zeros_like(xt))
+        eng.set_spread_merge(c)
+        eng.deposit()
+        eng.solve_fields()
+        got[c] = eng.rho.cpu().numpy()
+        used = eng.spread_merge_used()
+        if c >= 2:
+            assert used == c
+        elif c == 0:
+            assert used == 1
+        else:   # by density, and never while the spread feeds the gather's weight cache
+            assert used == (1 if eng.weight_cache else 4 if ppc < 3 else 2)
+        assert rel_l2(got[c], rho_o) <= TIGHT, (c, rel_l2(got[c], rho_o))
+    assert rel_l2(got[2], got[0]) <= 1e-13 and rel_l2(got[4], got[0]) <= 1e-13
