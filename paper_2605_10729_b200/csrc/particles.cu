@@ -1127,9 +1127,6 @@ __device__ unsigned long long g_phase_cycles[8];
 #define PHASE_ADD(slot, a, b)
 #endif
 
-#ifndef PIF_SPARSE_PLANE_DEPTH
-#define PIF_SPARSE_PLANE_DEPTH 4
-#endif
 #ifndef PIF_INTERP_MINB
 #define PIF_INTERP_MINB 2
 #endif
@@ -1146,10 +1143,6 @@ constexpr int kGatherFmaMax = PIF_GATHER_FMA_MAX;
 #define PIF_GATHER_WARPS 4
 #endif
 constexpr int kGatherWarps = PIF_GATHER_WARPS;   // warps per gather block
-// dynamic shared memory of interp_mma_kernel: the per-warp partial sums, then
-// (WC) the second weight stage or (sparse: LONGSEG without WC) the plane ring
-constexpr int kGatherDynFixed = (int)(kGatherWarps * sizeof(GatherPartials));
-constexpr int kPlaneRingBytes = kGatherWarps * PIF_SPARSE_PLANE_DEPTH * 64 * (int)sizeof(double4);
 
 // WC: the window weights come from the spread's cache (pif_set_weight_cache)
 // instead of being evaluated here; a separate instantiation so the polynomial
@@ -1169,12 +1162,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                   const double *__restrict__ wc, int64_t wstride) {
     const int nitems = *n_items;
     __shared__ WarpChunk stage[kGatherWarps];
-    // footprint planes prefetched ahead of the walk: one cell step ahead, or
-    // PD steps (a ring of planes) on sparse sets, where a cell step holds too
-    // little work to cover one plane's memory latency
-    // (the ring lives in dynamic shared memory after the partials)
-    constexpr int PD = (LONGSEG && !WC) ? PIF_SPARSE_PLANE_DEPTH : 1;
-    __shared__ double4 planes[PD == 1 ? kGatherWarps : 1][8][8];
+    __shared__ double4 planes[kGatherWarps][8][8];
     __shared__ double tab[32];
     // this item's cell boundaries: one per lane in a register (segments of
     // <= 31 cells), or a per-warp shared table (LONGSEG: up to kMaxSeg cells)
@@ -1191,12 +1179,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
     // with the weight cache, chunks alternate between two stages (the next
     // chunk's weights land by cp.async while this one is gathered)
     WarpChunk &st1 = WC ? stage2[threadIdx.x >> 5] : st0;
-    double4 (*pring)[8][8] =
-        PD == 1 ? reinterpret_cast<double4 (*)[8][8]>(planes[threadIdx.x >> 5])
-                : reinterpret_cast<double4 (*)[8][8]>(reinterpret_cast<char *>(dyn_smem) +
-                                                       kGatherDynFixed) +
-                      (threadIdx.x >> 5) * PD;
-    double4 (*pf)[8] = pring[0];
+    double4 (*pf)[8] = planes[threadIdx.x >> 5];
     chunk_zero(st0, lane);
     if (WC) chunk_zero(st1, lane);
     int wb = 0;            // stage of the current chunk
@@ -1273,13 +1256,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
             chunk_weights_async<W>(wb ? st1 : st0, wc, wstride, pbeg + lane, lane,
                                    min(kChunk, pend - pbeg));
         }
-        if (PD > 1) {
-#pragma unroll
-            for (int d = 0; d < PD; ++d)
-                prefetch_plane(pring[(kf + 8 + d) % PD], field, ix, iy, n, (kf + 8 + d) % n, lane);
-        } else {
-            prefetch_plane(pf, field, ix, iy, n, (kf + 8) % n, lane);
-        }
+        prefetch_plane(pf, field, ix, iy, n, (kf + 8) % n, lane);
         wnewest = false;
 
         for (int pos = pbeg; pos < pend; pos += kChunk) {
@@ -1323,22 +1300,6 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                 const int gp = pos + j;
                 if (gp >= cell_end) {   // next cell: plane k leaves slot k&7, plane k+8 enters
                     const int s = k & 7;
-                    if (PD > 1) {
-                        // plane k+8 is the oldest of the PD groups in flight
-                        asm volatile("cp.async.wait_group %0;" ::"n"(PD - 1) : "memory");
-                        __syncwarp();
-                        double4 (*pk)[8] = pring[(k + 8) % PD];
-                        if (c4 == (s & 3)) {
-                            if (s >> 2) plane_from_smem(g, 1, pk, r);
-                            else plane_from_smem(g, 0, pk, r);
-                        }
-                        __syncwarp();
-                        // its ring slot takes plane k+8+PD
-                        prefetch_plane(pk, field, ix, iy, n, (k + 8 + PD) % n, lane);
-                        ++k;
-                        cell_end = bound(k - k0 + 1);
-                        continue;
-                    }
                     if (wnewest) {   // the plane group is older than the weights group
                         asm volatile("cp.async.wait_group 1;" ::: "memory");
                         __syncwarp();
@@ -2622,11 +2583,8 @@ int launch_spread(Plan &p, const pif_soa_t &P, const int32_t *perm, const double
 
 // dynamic shared memory of interp_mma_kernel: the per-warp partial sums (+ the
 // second weight stage when the weight cache is in use)
-constexpr int kGatherDyn = kGatherDynFixed;
-constexpr int kGatherDynMax =
-    kGatherDyn + ((int)(kGatherWarps * sizeof(WarpChunk)) > kPlaneRingBytes
-                      ? (int)(kGatherWarps * sizeof(WarpChunk))
-                      : kPlaneRingBytes);
+constexpr int kGatherDyn = (int)(kGatherWarps * sizeof(GatherPartials));
+constexpr int kGatherDynMax = kGatherDyn + (int)(kGatherWarps * sizeof(WarpChunk));
 
 // spread -> gather window-weight cache, [24][M] doubles, grown on demand
 int ensure_wcache(Plan &p, int64_t M) {
@@ -2670,10 +2628,9 @@ int interp_impl(Plan &p, const pif_soa_t &P, const int32_t *perm, pif_soa_t &Q, 
                             p.wcache_perm == perm && p.wcache_count == P.count)
                                ? p.wcache
                                : nullptr;
-        const bool longseg = p.seg > 31;
-        const size_t dyn = kGatherDyn + (wc ? kGatherWarps * sizeof(WarpChunk)
-                                            : (longseg ? (size_t)kPlaneRingBytes : 0));
+        const size_t dyn = kGatherDyn + (wc ? kGatherWarps * sizeof(WarpChunk) : 0);
         const int gthreads = kGatherWarps * 32;
+        const bool longseg = p.seg > 31;
 #define PIF_INTERP_CASE(W)                                                                    \
     case W: {                                                                                 \
         if (push) {                                                                           \
