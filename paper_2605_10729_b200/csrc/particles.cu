@@ -246,6 +246,10 @@ constexpr int kChunk = 32;
 #ifndef PIF_GATHER_CHAINS
 #define PIF_GATHER_CHAINS 3
 #endif
+// the FMA path handles particles in pairs (1) or one at a time (0)
+#ifndef PIF_GATHER_FMA_PAIRS
+#define PIF_GATHER_FMA_PAIRS 1
+#endif
 
 // Layouts chosen so the hot shared-memory accesses are bank-conflict free
 // (64-bit words, 16 per half-warp phase): wz is [c][p] with row stride 36
@@ -1038,7 +1042,49 @@ __device__ __forceinline__ void gather_sub_fma(WarpChunk &st, GatherPartials &gp
                                                const double (&g)[8][2][3], int j, int m, int k,
                                                int r, int c4) {
     const int s0 = (c4 - k) & 7, s1 = (c4 + 4 - k) & 7;
-    for (int q = j; q < j + m; ++q) {
+    int q = j;
+#if PIF_GATHER_FMA_PAIRS
+    // two particles at a time: 12 independent FMA chains and 6 shuffle
+    // reductions in flight instead of 6 and 3 (sparse sets run almost all
+    // their particles here); each particle's arithmetic is unchanged
+    for (; q + 2 <= j + m; q += 2) {
+        double h0[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+        double h1[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const double xa = st.wx[a][q], xb = st.wx[a][q + 1];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                h0[0][d] = fma(g[a][0][d], xa, h0[0][d]);
+                h1[0][d] = fma(g[a][1][d], xa, h1[0][d]);
+                h0[1][d] = fma(g[a][0][d], xb, h0[1][d]);
+                h1[1][d] = fma(g[a][1][d], xb, h1[1][d]);
+            }
+        }
+        double e[2][3];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const double z0 = st.wz[s0][q + u], z1 = st.wz[s1][q + u];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) e[u][d] = fma(h1[u][d], z1, h0[u][d] * z0);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) e[u][d] += __shfl_xor_sync(kFull, e[u][d], 1);
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+            for (int d = 0; d < 3; ++d) e[u][d] += __shfl_xor_sync(kFull, e[u][d], 2);
+        if (c4 == 0) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int d = 0; d < 3; ++d) gp.D[d][r][q + u] = e[u][d];
+        }
+    }
+#endif
+    for (; q < j + m; ++q) {
         double h0[3] = {0.0, 0.0, 0.0}, h1[3] = {0.0, 0.0, 0.0};
 #pragma unroll
         for (int a = 0; a < 8; ++a) {
