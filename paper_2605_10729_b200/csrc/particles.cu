@@ -246,10 +246,6 @@ constexpr int kChunk = 32;
 #ifndef PIF_GATHER_CHAINS
 #define PIF_GATHER_CHAINS 3
 #endif
-// the FMA path handles particles in pairs (1) or one at a time (0)
-#ifndef PIF_GATHER_FMA_PAIRS
-#define PIF_GATHER_FMA_PAIRS 1
-#endif
 
 // Layouts chosen so the hot shared-memory accesses are bank-conflict free
 // (64-bit words, 16 per half-warp phase): wz is [c][p] with row stride 36
@@ -1038,16 +1034,17 @@ __device__ __forceinline__ void gather_sub_d(WarpChunk &st, GatherPartials &gp,
 // particle and the 4 lanes of row r reduce, giving the same D_d[p][b] as
 // gather_sub_d.  Pipe cost ~54 FMAs per particle against 48 DMMAs per
 // sub-batch, so partial sub-batches (cell tails, sparse cells) run here.
+template <bool PAIRS>
 __device__ __forceinline__ void gather_sub_fma(WarpChunk &st, GatherPartials &gp,
                                                const double (&g)[8][2][3], int j, int m, int k,
                                                int r, int c4) {
     const int s0 = (c4 - k) & 7, s1 = (c4 + 4 - k) & 7;
     int q = j;
-#if PIF_GATHER_FMA_PAIRS
-    // two particles at a time: 12 independent FMA chains and 6 shuffle
-    // reductions in flight instead of 6 and 3 (sparse sets run almost all
-    // their particles here); each particle's arithmetic is unchanged
-    for (; q + 2 <= j + m; q += 2) {
+    // PAIRS (sparse sets, which run almost all their particles here): two
+    // particles at a time, 12 independent FMA chains and 6 shuffle reductions
+    // in flight instead of 6 and 3; each particle's arithmetic is unchanged
+    // (256^3 / 1.25 per cell: gather -1.5%; dense sets: +1%, so not there)
+    for (; PAIRS && q + 2 <= j + m; q += 2) {
         double h0[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
         double h1[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
 #pragma unroll
@@ -1083,7 +1080,6 @@ __device__ __forceinline__ void gather_sub_fma(WarpChunk &st, GatherPartials &gp
                 for (int d = 0; d < 3; ++d) gp.D[d][r][q + u] = e[u][d];
         }
     }
-#endif
     for (; q < j + m; ++q) {
         double h0[3] = {0.0, 0.0, 0.0}, h1[3] = {0.0, 0.0, 0.0};
 #pragma unroll
@@ -1365,7 +1361,7 @@ interp_mma_kernel(pif_soa_t P, const int32_t *__restrict__ perm, pif_soa_t Q,
                 }
                 const int m = min(8, min(pos + cnt, cell_end) - gp);
                 PIF_CHECK(m > 0 && j + m <= kChunk && k >= k0 && k < k1);
-                if (m <= kGatherFmaMax) gather_sub_fma(st, gpart, g, j, m, k, r, c4);
+                if (m <= kGatherFmaMax) gather_sub_fma<LONGSEG>(st, gpart, g, j, m, k, r, c4);
                 else gather_sub_d(st, gpart, g, j, m, k, r, c4);
                 j += m;
             }
