@@ -416,6 +416,31 @@ def run_b200(a):
         dist.destroy_process_group()
 
 
+def pin_near_gpu(torch, dev):
+    """Move this rank onto the host CPUs local to its GPU (sysfs local_cpulist
+    of the GPU's PCI function) while the pinned staging is allocated, so its
+    pages land on the GPU's NUMA node and the copies do not cross sockets (the
+    caller restores the affinity).  Returns the CPU list (None when the
+    topology is not visible).  PIF_E2E_NUMA=0 skips it."""
+    if os.environ.get("PIF_E2E_NUMA", "1") != "1":
+        return None
+    try:
+        pr = torch.cuda.get_device_properties(dev)
+        bdf = f"{pr.pci_domain_id:04x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bdf}/local_cpulist") as f:
+            spec = f.read().strip()
+        cpus = set()
+        for part in spec.split(","):
+            lo_, _, hi_ = part.partition("-")
+            cpus.update(range(int(lo_), int(hi_ or lo_) + 1))
+        if cpus and cpus != set(range(os.cpu_count() or 0)):
+            os.sched_setaffinity(0, cpus)
+            return spec
+        return None
+    except Exception:  # noqa: BLE001 - topology not visible: leave placement alone
+        return None
+
+
 def run_e2e(a, eng, torch, dist, world, per_gpu, glob, dev):
     """pif_step-style use with host (pinned) particle arrays in id order (the
     reference's ParticleEnsemble layout) through PifEngine.run_host: per step
@@ -436,8 +461,11 @@ def run_e2e(a, eng, torch, dist, world, per_gpu, glob, dev):
                 "skipped": f"host memory: {need / 1e9:.0f} GB pinned needed, "
                            f"{avail / 1e9:.0f} GB available"}
     lo = int(eng.parts.ids[eng.parts.cur][:M].min())
+    cpus0 = os.sched_getaffinity(0)
+    numa = pin_near_gpu(torch, dev)
     xh = torch.empty((M, 3), dtype=torch.float64, pin_memory=True)
     vh = torch.empty((M, 3), dtype=torch.float64, pin_memory=True)
+    os.sched_setaffinity(0, cpus0)      # pages are placed; the CPU arm keeps every core
     xd, vd = eng.to_id_order(id0=lo)
     xh.copy_(xd)
     vh.copy_(vd)
@@ -467,7 +495,7 @@ def run_e2e(a, eng, torch, dist, world, per_gpu, glob, dev):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         T = float(tt[0])
     return {"value": glob * K / T, "unit": UNIT, "h2d_bytes_per_step": M * 48 * world,
-            "d2h_bytes_per_step": (M * 48 + 8) * world, "steps": K,
+            "d2h_bytes_per_step": (M * 48 + 8) * world, "steps": K, "host_cpus": numa,
             "api": "PifEngine.run_host (pif_step-style): per step H2D x,v (pinned, id order) -> "
                    "fused AoS load/wrap/keys + bin -> deposit -> allreduce -> solve_fields -> "
                    "gather+push (also writing x,v in id order) -> D2H x,v,W; step s's D2H and "
