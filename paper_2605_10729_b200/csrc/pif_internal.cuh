@@ -65,9 +65,6 @@ struct Plan {
     double *mirror_x = nullptr;    // id-order (M,3) mirrors written by the push kernels
     double *mirror_v = nullptr;
     long long mirror_id0 = 0;
-    // split step (pif_interp_split / pif_push_ids): E rows in id order in
-    // ring_scratch, valid for split_count rows; split_parts diagnostic
-    // partial blocks used by the row chunks pushed so far
     // merged-column spread for sparse sets (spread_merged_kernel): C adjacent
     // x columns walked as one super-column in their own cell order
     // (cell_start2 / perm2 / items2, derived from the standard binning at each
@@ -75,13 +72,16 @@ struct Plan {
     // (pif_set_spread_merge, PIF_SPREAD_MERGE)
     int merge_force = -1;
     int merge_used = 1;            // C of the last spread (1: standard kernel)
-    int32_t *cell_start2 = nullptr;  // n^3 + 1 (counts, then their scan)
+    int32_t *cell_start2 = nullptr;  // 2 (n^3 + 1): merged counts, then their scan
     int32_t *perm2 = nullptr;
     int64_t perm2_cap = 0;
     int2 *items2 = nullptr;
     int64_t items2_cap = 0;
     int *seg_parts2 = nullptr, *seg_off2 = nullptr;
     int64_t segs2_cap = 0;
+    // split step (pif_interp_split / pif_push_ids): E rows in id order in
+    // ring_scratch, valid for split_count rows; split_parts diagnostic
+    // partial blocks used by the row chunks pushed so far
     bool split_valid = false;
     int64_t split_count = 0;
     int split_parts = 0;
