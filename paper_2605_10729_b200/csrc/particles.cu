@@ -161,25 +161,42 @@ __global__ void bin_perm_kernel(const int32_t *__restrict__ key, const int32_t *
 // rank-free variant: the in-cell slot comes from a cursor per cell (the count
 // table, zeroed after the scan); lanes of a warp holding the same key take
 // consecutive slots with one atomic (consecutive particles mostly share a
-// cell: they were written in cell order by the previous push)
+// cell: they were written in cell order by the previous push).  Each warp
+// takes kPermUnroll x 32 consecutive particles per pass so that many cursor
+// atomics are in flight at once (the pass is bound by their round trips).
+constexpr int kPermUnroll = 4;
 __global__ void bin_perm_cursor_kernel(const int32_t *__restrict__ key, int32_t *__restrict__ cursor,
                                        const int32_t *__restrict__ start, int64_t M,
                                        int32_t *__restrict__ perm) {
     const int lane = threadIdx.x & 31;
-    for (int64_t j0 = blockIdx.x * (int64_t)blockDim.x; j0 < M;
-         j0 += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t j = j0 + threadIdx.x;
-        const bool ok = j < M;
-        const int k = ok ? key[j] : -1;
-        const unsigned peers = __match_any_sync(0xffffffffu, k);
-        const int leader = __ffs(peers) - 1;
-        int base = 0;
-        if (ok && lane == leader) base = atomicAdd(&cursor[k], __popc(peers));
-        base = __shfl_sync(peers, base, leader);
-        if (ok) {
-            const int slot = start[k] + base + __popc(peers & ((1u << lane) - 1u));
-            PIF_CHECK(slot >= 0 && slot < M);
-            perm[slot] = (int32_t)j;
+    const unsigned below = (1u << lane) - 1u;
+    const int64_t sweep = (int64_t)gridDim.x * blockDim.x * kPermUnroll;
+    for (int64_t b0 = ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) * kPermUnroll;
+         b0 < M; b0 += sweep) {
+        int k[kPermUnroll], base[kPermUnroll];
+        unsigned peers[kPermUnroll];
+#pragma unroll
+        for (int u = 0; u < kPermUnroll; ++u) {
+            const int64_t j = b0 + u * 32 + lane;
+            k[u] = j < M ? key[j] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < kPermUnroll; ++u) peers[u] = __match_any_sync(0xffffffffu, k[u]);
+#pragma unroll
+        for (int u = 0; u < kPermUnroll; ++u) {
+            base[u] = 0;
+            if (k[u] >= 0 && lane == __ffs(peers[u]) - 1)
+                base[u] = atomicAdd(&cursor[k[u]], __popc(peers[u]));
+        }
+#pragma unroll
+        for (int u = 0; u < kPermUnroll; ++u) {
+            base[u] = __shfl_sync(peers[u], base[u], __ffs(peers[u]) - 1);
+            if (k[u] >= 0) {
+                const int64_t j = b0 + u * 32 + lane;
+                const int slot = start[k[u]] + base[u] + __popc(peers[u] & below);
+                PIF_CHECK(slot >= 0 && slot < M);
+                perm[slot] = (int32_t)j;
+            }
         }
     }
 }
@@ -2380,7 +2397,8 @@ int launch_bin_perm(Plan &p, const int32_t *key, const int32_t *rank, int64_t M,
     } else if (M > 0) {
         e = cudaMemsetAsync(p.cell_count, 0, sizeof(int32_t) * (p.n3 + 1), s);
         if (e != cudaSuccess) return fail_cuda(e, "reset cell cursors");
-        bin_perm_cursor_kernel<<<grid_for(M, 256, p.sm_count), 256, 0, s>>>(
+        bin_perm_cursor_kernel<<<grid_for((M + kPermUnroll - 1) / kPermUnroll, 256, p.sm_count),
+                                 256, 0, s>>>(
             key, p.cell_count, p.cell_start, M, perm);
         e = cudaGetLastError();
         if (e != cudaSuccess) return fail_cuda(e, "bin_perm_cursor_kernel");
