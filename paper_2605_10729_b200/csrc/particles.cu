@@ -588,11 +588,6 @@ spread_mma_kernel(const double *__restrict__ px, const double *__restrict__ py,
 // merged spread (merged_counts / scan / merged_perm / merged_seg_parts).
 // ----------------------------------------------------------------------------
 
-__device__ __forceinline__ int64_t merged_cell(int k, int n, int C) {
-    const int kz = k % n, t = k / n, ky = t % n, kx = t / n;
-    return ((((int64_t)(kx / C) * n + ky) * n + kz) * C) + kx % C;
-}
-
 // count2[mk] = size of the standard cell behind merged cell mk; count2[n^3] = 0
 __global__ void merged_counts_kernel(const int32_t *__restrict__ cell_start, int n, int C,
                                      int32_t *__restrict__ count2) {
@@ -614,21 +609,25 @@ __global__ void merged_counts_kernel(const int32_t *__restrict__ cell_start, int
     }
 }
 
-// perm2: a standard cell's particles keep their slot order inside their merged
-// cell; the cell comes from the particle's position (the binning's own key)
-__global__ void merged_perm_kernel(const double *__restrict__ px, const double *__restrict__ py,
-                                   const double *__restrict__ pz,
-                                   const int32_t *__restrict__ perm,
+// perm2: each merged cell mk copies the perm run of its standard cell k (same
+// particles, same order); one thread per merged cell, so perm2 is written in
+// order and nothing but the two cell tables and perm is read
+__global__ void merged_perm_kernel(const int32_t *__restrict__ perm,
                                    const int32_t *__restrict__ cell_start,
-                                   const int32_t *__restrict__ cell_start2, int64_t M, double h,
-                                   int w, int n, int C, int32_t *__restrict__ perm2) {
-    const double rh = __drcp_rn(h);
-    for (int64_t slot = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; slot < M;
-         slot += (int64_t)gridDim.x * blockDim.x) {
-        const int j = perm ? perm[slot] : (int)slot;
-        const int k = cell_key(px[j], py[j], pz[j], h, rh, w, n);
-        PIF_CHECK(slot >= cell_start[k] && slot < cell_start[k + 1]);
-        perm2[cell_start2[merged_cell(k, n, C)] + (slot - cell_start[k])] = j;
+                                   const int32_t *__restrict__ cell_start2, int n, int C,
+                                   int32_t *__restrict__ perm2) {
+    const int64_t n3 = (int64_t)n * n * n;
+    for (int64_t mk = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; mk < n3;
+         mk += (int64_t)gridDim.x * blockDim.x) {
+        const int q = (int)(mk % C);
+        int64_t t = mk / C;
+        const int kz = (int)(t % n);
+        t /= n;
+        const int ky = (int)(t % n);
+        const int mx = (int)(t / n);
+        const int64_t k = ((int64_t)(mx * C + q) * n + ky) * n + kz;
+        const int src = cell_start[k], cnt = cell_start[k + 1] - src, dst = cell_start2[mk];
+        for (int i = 0; i < cnt; ++i) perm2[dst + i] = perm ? perm[src + i] : src + i;
     }
 }
 
@@ -2461,8 +2460,8 @@ int build_merged(Plan &p, const pif_soa_t &P, const int32_t *perm, int C, int &s
     size_t tmp = p.scan_tmp_bytes;
     cudaError_t e = cub::DeviceScan::ExclusiveSum(p.scan_tmp, tmp, count2, cs2, (int)(n3 + 1), s);
     if (e != cudaSuccess) return fail_cuda(e, "merged cell scan");
-    merged_perm_kernel<<<grid_for(M, 256, p.sm_count), 256, 0, s>>>(
-        P.x, P.y, P.z, perm, p.cell_start, cs2, M, p.h, p.w, p.n, C, p.perm2);
+    merged_perm_kernel<<<grid_for(n3, 256, p.sm_count), 256, 0, s>>>(perm, p.cell_start, cs2, p.n,
+                                                                    C, p.perm2);
     // segments of seg levels holding ~seg_target particles, as segment_cells
     const double per_level = p.density * C;
     seg = (int)std::ceil((double)p.seg_target / (per_level > 1.0 ? per_level : 1.0));
