@@ -610,24 +610,44 @@ __global__ void merged_counts_kernel(const int32_t *__restrict__ cell_start, int
 }
 
 // perm2: each merged cell mk copies the perm run of its standard cell k (same
-// particles, same order); one thread per merged cell, so perm2 is written in
-// order and nothing but the two cell tables and perm is read
+// particles, same order): one lane per merged cell for the first 16 entries,
+// the whole warp for the rest of heavy cells (a Penning core cell holds
+// thousands), so perm2 is written nearly in order and only the two cell
+// tables and perm are read
 __global__ void merged_perm_kernel(const int32_t *__restrict__ perm,
                                    const int32_t *__restrict__ cell_start,
                                    const int32_t *__restrict__ cell_start2, int n, int C,
                                    int32_t *__restrict__ perm2) {
+    constexpr int kLight = 16;
     const int64_t n3 = (int64_t)n * n * n;
-    for (int64_t mk = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; mk < n3;
-         mk += (int64_t)gridDim.x * blockDim.x) {
-        const int q = (int)(mk % C);
-        int64_t t = mk / C;
-        const int kz = (int)(t % n);
-        t /= n;
-        const int ky = (int)(t % n);
-        const int mx = (int)(t / n);
-        const int64_t k = ((int64_t)(mx * C + q) * n + ky) * n + kz;
-        const int src = cell_start[k], cnt = cell_start[k + 1] - src, dst = cell_start2[mk];
-        for (int i = 0; i < cnt; ++i) perm2[dst + i] = perm ? perm[src + i] : src + i;
+    const int lane = threadIdx.x & 31;
+    const int64_t sweep = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t w0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); w0 < n3;
+         w0 += sweep) {   // warp-uniform trip count
+        const int64_t mk = w0 + lane;
+        int src = 0, cnt = 0, dst = 0;
+        if (mk < n3) {
+            const int q = (int)(mk % C);
+            int64_t t = mk / C;
+            const int kz = (int)(t % n);
+            t /= n;
+            const int ky = (int)(t % n);
+            const int mx = (int)(t / n);
+            const int64_t k = ((int64_t)(mx * C + q) * n + ky) * n + kz;
+            src = cell_start[k];
+            cnt = cell_start[k + 1] - src;
+            dst = cell_start2[mk];
+        }
+        for (int i = 0; i < min(cnt, kLight); ++i) perm2[dst + i] = perm ? perm[src + i] : src + i;
+        unsigned heavy = __ballot_sync(0xffffffffu, cnt > kLight);
+        while (heavy) {
+            const int h = __ffs(heavy) - 1;
+            heavy &= heavy - 1u;
+            const int hs = __shfl_sync(0xffffffffu, src, h), hc = __shfl_sync(0xffffffffu, cnt, h),
+                      hd = __shfl_sync(0xffffffffu, dst, h);
+            for (int i = kLight + lane; i < hc; i += 32)
+                perm2[hd + i] = perm ? perm[hs + i] : hs + i;
+        }
     }
 }
 
