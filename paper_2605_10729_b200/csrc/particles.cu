@@ -2446,6 +2446,10 @@ int merged_factor(const Plan &p) {
     // the column order), and from 4 per cell the cache is worth more (128^3 /
     // 8 per cell: spread -1.0 ms merged, gather +1.9 ms without the cache)
     if (p.wcache_on) return 1;
+    // heavy cells (the push_agg decision: some segment holds >= 12 work
+    // items): the merged walk only adds DMMAs there (clustered 64^3 / 2^24:
+    // 1.21 -> 1.87 ms merged; profiles/round2/microbench_merge_ab.md)
+    if (p.push_agg) return 1;
     if (p.density < PIF_MERGE4_BELOW) return 4;
     if (p.density < PIF_MERGE2_BELOW) return 2;
     return 1;
