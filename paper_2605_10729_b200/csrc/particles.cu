@@ -425,8 +425,10 @@ __device__ __forceinline__ void spread_flush_plane(double (&acc)[8][2], int k, i
     }
 }
 
+// k-steps unrolled in the spread's DMMA loop (4: 9.24 -> 9.16 ms at 2^27
+// against 2, profiles/round2/spread_knobs_ab.txt)
 #ifndef PIF_SPREAD_UNROLL
-#define PIF_SPREAD_UNROLL 2
+#define PIF_SPREAD_UNROLL 4
 #endif
 constexpr int kSpreadUnroll = PIF_SPREAD_UNROLL;
 #ifndef PIF_SPREAD_MINB
